@@ -1,0 +1,279 @@
+/*
+ * rlo.h — C ABI of the B200-native RL-objective hot path ("rlo" = ROLL objective).
+ *
+ * This is the drop-in boundary for the per-token RL objective that the ROLL
+ * reference ("rollmini", /root/reference/proj) computes on the CPU between
+ * generation and the actor update.  Every entry point names the reference
+ * interface it replaces (file:line, relative to proj/core/).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no C++ / torch types cross this boundary.
+ *  - Device pointers (suffix "device" in the comments) must be CUDA device
+ *    memory of the handle's device.  The caller owns every buffer.
+ *  - Calls taking a `stream` are asynchronous, stream-ordered on that
+ *    cudaStream_t (NULL = legacy default stream), unless documented to sync.
+ *  - One handle per (device, host thread, stream): the handle owns scratch
+ *    workspace exactly like the reference's one PolicyWorkspace per worker
+ *    (include/rollmini/policy_workers.hpp:41).
+ *  - Errors are status codes; the message of the last failure on the calling
+ *    thread is returned by rlo_last_error().  The codes map 1:1 onto the
+ *    reference exception classes (include/rollmini/errors.hpp:11-82).
+ *
+ * Batch layout (the padded form of SampleBatch, include/rollmini/sample.hpp:16-60):
+ *  B sequences, row stride T.  Per-token arrays are [B*T], token (b,t) at
+ *  index b*T+t, valid iff t < lengths[b].  A NULL mask means "every response
+ *  token participates" (the empty action_mask of sample.hpp:31).
+ *  Logits row for token (b,t) starts at data + (b*T+t)*row_stride elements.
+ */
+#ifndef RLO_H_
+#define RLO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RLO_ABI_VERSION 1
+
+/* Status codes — reference exception taxonomy (include/rollmini/errors.hpp). */
+typedef enum rlo_status {
+  RLO_OK = 0,
+  RLO_ERR_INPUT = 1,    /* InputError    errors.hpp:33-37: OOV tokens, missing rewards/advantages/logprobs */
+  RLO_ERR_CONFIG = 2,   /* ConfigError   errors.hpp:21-25: TrainConfig::validate, policy.cpp:29-37 */
+  RLO_ERR_TRAINING = 3, /* TrainingError errors.hpp:65-69: zero tokens / non-finite loss or gradient */
+  RLO_ERR_CUDA = 4,     /* device failure (no reference counterpart) */
+  RLO_ERR_NCCL = 5,     /* collective failure; the reference's CollectError (errors.hpp:51-57) */
+  RLO_ERR_DISPATCH = 6  /* DispatchError errors.hpp:39-43: unknown method name */
+} rlo_status;
+
+typedef enum rlo_dtype { RLO_DTYPE_F32 = 0, RLO_DTYPE_BF16 = 1 } rlo_dtype;
+
+typedef enum rlo_adv_estimator {
+  RLO_ADV_REINFORCE = 0, /* reference compute_advantages, policy.cpp:257-311 */
+  RLO_ADV_GRPO = 1,      /* group-normalised sequence reward */
+  RLO_ADV_GAE = 2        /* generalised advantage estimation over critic values */
+} rlo_adv_estimator;
+
+typedef enum rlo_kl_estimator {
+  RLO_KL_K1 = 0, /* r = lp - ref_lp, the reference's term (policy.cpp:364-368) */
+  RLO_KL_K2 = 1, /* r^2 / 2 */
+  RLO_KL_K3 = 2  /* exp(-r) - 1 + r */
+} rlo_kl_estimator;
+
+typedef enum rlo_loss_agg {
+  RLO_AGG_TOKEN_MEAN = 0,          /* reference: sum / tokens (policy.cpp:437-443) */
+  RLO_AGG_SEQ_MEAN_TOKEN_MEAN = 1, /* GRPO sample-level mean */
+  RLO_AGG_SEQ_MEAN_TOKEN_SUM = 2,
+  RLO_AGG_GROUP_MEAN = 3           /* mean over groups of the group's token-mean */
+} rlo_loss_agg;
+
+/* TrainConfig (include/rollmini/policy.hpp:57-67) plus the ROLL extensions
+ * the north star asks for.  rlo_train_config_default() gives the reference
+ * defaults (policy.hpp:58-64; config keys config.cpp:197-205). */
+typedef struct rlo_train_config {
+  double clip_eps;          /* 0.2,  (0,1) */
+  double kl_coef;           /* 0.0,  >= 0 */
+  double learning_rate;     /* 0.05, >= 0 (validated for parity; the update is outside this path) */
+  double advantage_clip;    /* 10.0, > 0 */
+  double reward_clip;       /* 20.0, > 0 */
+  double gamma;             /* 1.0,  (0,1] */
+  int32_t whiten_advantages;/* 0 */
+  /* extensions */
+  int32_t adv_estimator;    /* rlo_adv_estimator, REINFORCE */
+  double lambd;             /* GAE lambda, 0.95, [0,1] */
+  int32_t kl_estimator;     /* rlo_kl_estimator, K1 */
+  double dual_clip_c;       /* 0 = off; otherwise > 1 (dual-clip PPO) */
+  int32_t loss_agg;         /* rlo_loss_agg, TOKEN_MEAN */
+  int32_t group_size;       /* G: GRPO group / group-mean aggregation, 1 */
+  int32_t grpo_std_ddof;    /* 0 (population std, like policy.cpp:301) or 1 */
+  double grpo_eps;          /* 1e-6 */
+} rlo_train_config;
+
+/* Padded device view of a SampleBatch. */
+typedef struct rlo_batch {
+  int32_t B;               /* sequences in this view */
+  int32_t T;               /* row stride of the per-token arrays */
+  int32_t seq_offset;      /* index of this view's first sequence in the rank-local batch (micro-batching) */
+  int32_t reserved;
+  const int32_t* lengths;  /* [B] device: response lengths, 0..T */
+  const int32_t* tokens;   /* [B*T] device: response_tokens (sample.hpp:21) */
+  const uint8_t* mask;     /* [B*T] device or NULL: action_mask (sample.hpp:26) */
+} rlo_batch;
+
+/* One model's logits over the batch rows. */
+typedef struct rlo_logits {
+  const void* data;        /* device; dtype elements */
+  int32_t dtype;           /* rlo_dtype */
+  int32_t V;               /* vocab size */
+  int64_t row_stride;      /* elements between consecutive rows (>= V) */
+} rlo_logits;
+
+/* Optional per-token outputs of rlo_ppo_gradient ([B*T] device, any may be NULL). */
+typedef struct rlo_token_out {
+  float* logp;      /* actor log-prob of the realised token */
+  float* old_logp;  /* old-policy log-prob (when computed from old logits) */
+  float* ref_logp;  /* reference log-prob (when computed from ref logits) */
+  float* entropy;   /* actor entropy of the position */
+  float* dlogp;     /* d(loss_t)/d(logp_t), policy.cpp:372-374 */
+  float* loss;      /* per-token loss contribution (0 for non-participating tokens) */
+} rlo_token_out;
+
+/* UpdateStats (include/rollmini/policy.hpp:130-136) plus extension stats. */
+typedef struct rlo_stats {
+  double loss;               /* aggregated per cfg.loss_agg */
+  double mean_ratio;
+  double clip_fraction;
+  double mean_kl;
+  uint64_t tokens;
+  double mean_entropy;       /* over loss-participating tokens */
+  double dual_clip_fraction;
+  uint64_t seqs;             /* sequences with >= 1 participating token */
+  uint64_t groups;           /* groups with >= 1 participating token */
+} rlo_stats;
+
+/* Per-rank partial sums: the scalar part of GradAccum (policy.hpp:121-128),
+ * extended.  Merged in rank order exactly like merge_gradients
+ * (policy.cpp:428-436).  Layout of v[] (all fp64; counts are exact integers): */
+#define RLO_NPARTIAL 16
+enum {
+  RLO_P_LOSS_SUM = 0,   /* sum of per-token loss */
+  RLO_P_RATIO_SUM = 1,
+  RLO_P_KL_SUM = 2,
+  RLO_P_ENTROPY_SUM = 3,
+  RLO_P_CLIPPED = 4,
+  RLO_P_DUAL_CLIPPED = 5,
+  RLO_P_TOKENS = 6,
+  RLO_P_SEQ_MEAN_SUM = 7,   /* sum over non-empty seqs of (seq loss sum / seq tokens) */
+  RLO_P_SEQS = 8,           /* non-empty sequences */
+  RLO_P_GROUP_MEAN_SUM = 9, /* sum over non-empty groups of (group loss sum / group tokens) */
+  RLO_P_GROUPS = 10,        /* non-empty groups */
+  RLO_P_NONFINITE_GRAD = 11,/* tokens whose dlogp is not finite */
+  RLO_P_NONFINITE_LOSS = 12
+};
+typedef struct rlo_partials { double v[RLO_NPARTIAL]; } rlo_partials;
+
+typedef struct rlo_handle rlo_handle;
+
+/* ---- library / config (host only; callable without a GPU) -------------- */
+int rlo_abi_version(void);
+const char* rlo_last_error(void);
+void rlo_train_config_default(rlo_train_config* cfg);
+/* TrainConfig::validate (policy.cpp:29-37), same messages; plus extensions. */
+rlo_status rlo_train_config_validate(const rlo_train_config* cfg);
+/* split_sizes (sample.hpp:51-53, sample.cpp:99-105): contiguous, larger first. */
+rlo_status rlo_split_sizes(int64_t n, int32_t parts, int64_t* out_sizes);
+/* Group-aligned data-parallel shard of B sequences in groups of G: the
+ * split_sizes rule applied to whole groups (G=1 reproduces split_batch,
+ * sample.cpp:107-116).  Returns this rank's first sequence and count. */
+rlo_status rlo_shard_plan(int32_t B, int32_t G, int32_t world, int32_t rank,
+                          int32_t* out_seq_begin, int32_t* out_seq_count);
+/* merge_gradients scalar part (policy.cpp:421-450): rank-ordered sum of
+ * `nranks` partials, then normalisation; TrainingError on zero tokens or
+ * non-finite values, with the reference's messages. */
+rlo_status rlo_merge_partials(const rlo_partials* parts, int32_t nranks,
+                              const rlo_train_config* cfg, rlo_stats* out);
+
+/* ---- handle ------------------------------------------------------------ */
+rlo_status rlo_create(int32_t device, rlo_handle** out);
+rlo_status rlo_destroy(rlo_handle* h);
+/* NCCL data-parallel group (ranks = GPUs of one node, one handle per rank).
+ * unique_id is 128 bytes from rlo_comm_unique_id on rank 0, shared by the caller. */
+rlo_status rlo_comm_unique_id(void* unique_id_128);
+rlo_status rlo_comm_init(rlo_handle* h, const void* unique_id_128, int32_t rank, int32_t world);
+/* Kernel launches issued by this library since load (process-wide). */
+uint64_t rlo_launch_count(void);
+
+/* ---- the path ---------------------------------------------------------- */
+
+/* forward_logprobs (policy.hpp:107-109, policy.cpp:210-233): log-softmax of
+ * every valid response position (mask ignored, as the reference) gathered at
+ * the realised token.  Single pass over each logits row (online
+ * log-sum-exp); the softmax is never written.  Out-of-vocabulary tokens are
+ * reported as RLO_ERR_INPUT by the next synchronising call (rlo_sync or
+ * rlo_merge_gradients), with the reference message (policy.cpp:224-225).
+ * out_logp required; out_entropy / out_token_logit optional.  Invalid
+ * positions (t >= length) are written as 0. */
+rlo_status rlo_forward_logprobs(rlo_handle* h, const rlo_batch* batch, const rlo_logits* logits,
+                                float* out_logp, float* out_entropy, float* out_token_logit,
+                                void* stream);
+
+/* compute_advantages (policy.hpp:114-118, policy.cpp:257-311) and the ROLL
+ * estimators.  Rewards: rewards_tok [B*T] (per-token, sample.hpp:24) or
+ * rewards_seq [B] (scalar_reward, placed on the last token for
+ * REINFORCE/GAE); values [B*T] for GAE.  With a communicator, the whitening
+ * statistics are reduced over all ranks (NCCL all-gather + rank-ordered
+ * sum) on the stream.  out_adv [B*T] required; out_returns optional (GAE:
+ * A+V; REINFORCE: the discounted returns before whitening/clipping). */
+rlo_status rlo_compute_advantages(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch,
+                                  const float* rewards_tok, const float* rewards_seq,
+                                  const float* values, float* out_adv, float* out_returns,
+                                  void* stream);
+
+/* ppo_gradient loss part (policy.hpp:138-141, policy.cpp:313-374): fused
+ * single pass over the actor logits (and, when given, the old-policy and
+ * reference logits) computing log-probs, entropy, ratio, clip / dual-clip,
+ * KL (k1/k2/k3), per-token loss and dlogp for every loss-participating
+ * token.  Old / ref log-probs come from `old_logits` / `ref_logits` when
+ * non-NULL, else from `old_logp` / `ref_logp` [B*T] (sampling-time
+ * response_logprobs and ref_logprobs, sample.hpp:22-23).  ref may be absent
+ * entirely (no KL), unless kl_coef > 0 (InputError, policy.cpp:342-343).
+ * Per-sequence partial sums are accumulated in the handle (micro-batches:
+ * call repeatedly with batch->seq_offset) until rlo_merge_gradients. */
+rlo_status rlo_ppo_gradient(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch,
+                            const rlo_logits* actor_logits, const rlo_logits* old_logits,
+                            const rlo_logits* ref_logits, const float* old_logp,
+                            const float* ref_logp, const float* advantages,
+                            const rlo_token_out* out, void* stream);
+
+/* merge_gradients (policy.hpp:143-145, policy.cpp:421-450): reduces the
+ * accumulated per-sequence sums in a fixed order into this rank's partials,
+ * all-gathers them over the communicator (if any), merges in rank order and
+ * normalises per cfg.loss_agg.  Synchronises `stream`; resets the
+ * accumulator.  out_partials (this rank's, optional) may be NULL. */
+rlo_status rlo_merge_gradients(rlo_handle* h, const rlo_train_config* cfg, rlo_stats* out,
+                               rlo_partials* out_partials, void* stream);
+
+/* The whole path for one step (compute_advantages -> ppo_gradient ->
+ * merge_gradients) on device-resident inputs. */
+rlo_status rlo_objective_step(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch,
+                              const float* rewards_tok, const float* rewards_seq, const float* values,
+                              const rlo_logits* actor_logits, const rlo_logits* old_logits,
+                              const rlo_logits* ref_logits, const float* old_logp, const float* ref_logp,
+                              float* out_adv, const rlo_token_out* out, rlo_stats* stats,
+                              void* stream);
+
+/* Host-buffer form of rlo_objective_step, the reference-facing call: the
+ * SampleBatch arrays live in (preferably pinned) host memory and are copied
+ * to device inside the call; advantages and actor log-probs are copied back.
+ * Logits stay device-resident (they are the model's on-device output).
+ * Host pointers: lengths [B]; tokens [B*T]; mask [B*T] or NULL; rewards_tok
+ * [B*T] or NULL; rewards_seq [B] or NULL; values [B*T] or NULL; old_logp /
+ * ref_logp [B*T] or NULL; host_adv_out / host_logp_out [B*T] or NULL.
+ * Synchronises `stream`. */
+rlo_status rlo_objective_step_host(rlo_handle* h, const rlo_train_config* cfg, int32_t B, int32_t T,
+                                   const int32_t* lengths, const int32_t* tokens, const uint8_t* mask,
+                                   const float* rewards_tok, const float* rewards_seq,
+                                   const float* values, const rlo_logits* actor_logits,
+                                   const rlo_logits* old_logits, const rlo_logits* ref_logits,
+                                   const float* old_logp, const float* ref_logp,
+                                   float* host_adv_out, float* host_logp_out, rlo_stats* stats,
+                                   void* stream);
+
+/* Synchronise `stream` and report device-side input errors (OOV tokens). */
+rlo_status rlo_sync(rlo_handle* h, void* stream);
+
+/* ---- synthetic inputs (bench / tests; not on the path) ------------------ */
+/* Counter-hash logits identical to oracle/ synth twin: row r of model m is a
+ * pure function of (seed, m, r mod key_rows) — see DESIGN.md §synthetic. */
+rlo_status rlo_synth_logits(void* dst, int32_t dtype, int64_t rows, int32_t V, int64_t row_stride,
+                            uint64_t seed, int32_t model_id, int64_t row_key_offset, void* stream);
+rlo_status rlo_synth_tokens(int32_t* dst, int64_t rows, int32_t V, uint64_t seed,
+                            int64_t row_key_offset, int64_t key_rows, void* stream);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* RLO_H_ */
