@@ -35,6 +35,10 @@
 extern "C" {
 #endif
 
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the library is built -fvisibility=hidden; export exactly this header */
+#endif
+
 #define RLO_ABI_VERSION 1
 
 /* Status codes — reference exception taxonomy (include/rollmini/errors.hpp). */
@@ -271,6 +275,10 @@ rlo_status rlo_synth_logits(void* dst, int32_t dtype, int64_t rows, int32_t V, i
                             uint64_t seed, int32_t model_id, int64_t row_key_offset, void* stream);
 rlo_status rlo_synth_tokens(int32_t* dst, int64_t rows, int32_t V, uint64_t seed,
                             int64_t row_key_offset, int64_t key_rows, void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
 
 #ifdef __cplusplus
 } /* extern "C" */

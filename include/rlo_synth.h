@@ -60,7 +60,7 @@ RLO_HD int32_t rlo_synth_token(uint64_t seed, uint64_t row_key, int32_t V) {
   return (int32_t)((u >> 8) % (uint64_t)V);
 }
 
-#if defined(__CUDACC__)
+#if defined(__CUDA_ARCH__)
 #define RLO_FMUL(a, b) __fmul_rn((a), (b))
 #define RLO_FADD(a, b) __fadd_rn((a), (b))
 #else

@@ -1,0 +1,17 @@
+"""B200-native RL-objective hot path of ROLL (arXiv 2506.06122).
+
+The product is ``lib/librlo.so`` (C ABI in ``include/rlo.h``, sm_100a
+kernels in ``csrc/``).  This package mirrors the reference's host interface
+(``include/rollmini/policy.hpp``, ``worker.hpp``) on top of that ABI.
+"""
+from ._abi import LIB_PATH, declared_symbols  # noqa: F401
+from .errors import (CollectError, ConfigError, CudaError, DispatchError, Error, InputError,  # noqa: F401
+                     TrainingError)
+from .policy import (Message, Objective, PolicyWorker, TrainConfig, UpdateStats, launch_count,  # noqa: F401
+                     merge_partials, shard_plan, split_sizes, synth_logits, synth_tokens)
+
+__all__ = [
+    "Objective", "PolicyWorker", "Message", "TrainConfig", "UpdateStats", "split_sizes", "shard_plan",
+    "merge_partials", "launch_count", "synth_logits", "synth_tokens", "Error", "ConfigError", "InputError",
+    "TrainingError", "DispatchError", "CollectError", "CudaError",
+]

@@ -1,0 +1,112 @@
+// internal.h — declarations shared by the C-ABI host layer (api.cpp) and the
+// sm_100a kernels (*.cu).  Not installed; the public surface is include/rlo.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+
+#include "../../include/rlo.h"
+
+namespace rlo {
+
+extern std::atomic<uint64_t> g_launches;
+
+// Roles of the (up to 3) logits tensors a vocab pass reads.
+enum Role : int32_t { ROLE_ACTOR = 0, ROLE_OLD = 1, ROLE_REF = 2 };
+
+// Per-token flag bits written by the loss epilogue.
+enum : uint8_t { TF_CLIPPED = 1, TF_DUAL = 2, TF_NONFINITE_GRAD = 4, TF_NONFINITE_LOSS = 8 };
+
+// Device error slot: first failure wins (atomicCAS on code).
+enum : int32_t { DE_NONE = 0, DE_OOV_LOGPROB = 1, DE_OOV_LOSS = 2, DE_BAD_LENGTH = 3 };
+struct DevError {
+  int32_t code;
+  int32_t value;  // offending token id or sequence index
+};
+
+// Per-sequence record of the loss pass (fp64 sums in a fixed order).
+struct SeqRec {
+  double loss, ratio, kl, entropy;
+  double clipped, dual, tokens, nonfinite_grad, nonfinite_loss;
+  double pad;
+};
+
+// Per-slot whitening statistics (slot = sequence, or group for GRPO).
+struct WStat {
+  double sum, sq, count, pad;
+};
+
+struct VocabArgs {
+  const void* logits[3];
+  int64_t stride[3];
+  int32_t role[3];
+  int32_t ntens;
+  int32_t dtype;  // rlo_dtype shared by all tensors of the pass
+  int32_t V;
+  int32_t B, T;
+  const int32_t* lengths;
+  const int32_t* tokens;
+  const uint8_t* mask;
+  // forward_logprobs mode
+  float* out_lp;
+  float* out_ent;
+  float* out_tok;
+  // loss mode
+  const float* old_lp_in;
+  const float* ref_lp_in;
+  const float* adv;
+  double clip_eps, kl_coef, dual_c;
+  int32_t kl_est;
+  int32_t has_ref;  // KL term / kl_sum present (ref logits or ref_lp_in)
+  float* o_logp;
+  float* o_old;
+  float* o_ref;
+  float* o_ent;
+  float* o_dlogp;
+  float* o_loss;
+  // scratch consumed by the per-sequence reduction
+  float* s_loss;
+  float* s_ratio;
+  float* s_kl;
+  float* s_ent;
+  uint8_t* s_flags;
+  DevError* err;
+};
+
+struct AdvArgs {
+  int32_t B, T;
+  const int32_t* lengths;
+  const uint8_t* mask;
+  const float* rewards_tok;
+  const float* rewards_seq;
+  const float* values;
+  float* out_adv;
+  float* out_returns;
+  int32_t estimator;
+  double gamma, lambd, reward_clip, adv_clip;
+  int32_t whiten;
+  int32_t G, ddof;
+  double grpo_eps;
+  WStat* wstat;  // [B] (scan) or [B/G] (GRPO) when whiten
+};
+
+// Launchers (return cudaGetLastError()).
+cudaError_t launch_vocab_logprob(const VocabArgs& a, int num_sms, cudaStream_t s);
+cudaError_t launch_vocab_loss(const VocabArgs& a, int num_sms, cudaStream_t s);
+cudaError_t launch_seq_reduce(int32_t B, int32_t T, int32_t seq_offset, const int32_t* lengths,
+                              const uint8_t* mask, const float* s_loss, const float* s_ratio,
+                              const float* s_kl, const float* s_ent, const uint8_t* s_flags, SeqRec* recs,
+                              cudaStream_t s);
+cudaError_t launch_batch_reduce(const SeqRec* recs, int32_t nseq, int32_t G, double* partials,
+                                cudaStream_t s);
+cudaError_t launch_advantages(const AdvArgs& a, cudaStream_t s);
+cudaError_t launch_wstat_reduce(const WStat* w, int32_t n, double* out4, cudaStream_t s);
+cudaError_t launch_whiten_clip(const AdvArgs& a, const double* stats_all, int32_t world, cudaStream_t s);
+cudaError_t launch_synth_logits(void* dst, int32_t dtype, int64_t rows, int32_t V, int64_t row_stride,
+                                uint64_t seed, int32_t model_id, int64_t row_key_offset, cudaStream_t s);
+cudaError_t launch_synth_tokens(int32_t* dst, int64_t rows, int32_t V, uint64_t seed, int64_t row_key_offset,
+                                int64_t key_rows, cudaStream_t s);
+
+}  // namespace rlo

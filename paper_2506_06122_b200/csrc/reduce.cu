@@ -1,0 +1,129 @@
+// reduce.cu — K4: deterministic reductions of the loss pass.
+//
+// The reference accumulates GradAccum scalars in token order and merges
+// ranks in rank order (policy.cpp:366-370, :428-436; SPEC.md:278 fixed
+// reduction order).  Here: per-token results (vocab.cu) -> one warp per
+// sequence sums its tokens in fp64 (lane-strided + butterfly: a fixed order)
+// -> one CTA reduces the sequence records into the rank's partials, including
+// the sequence- and group-level aggregation sums.  No floating-point atomics
+// anywhere, so results are bitwise reproducible run to run.
+#include "common.cuh"
+#include "internal.h"
+
+namespace rlo {
+namespace {
+
+constexpr int kSeqWarps = 8;
+
+__global__ void __launch_bounds__(kSeqWarps * 32)
+    seq_reduce_kernel(int B, int T, int seq_offset, const int32_t* __restrict__ lengths,
+                      const uint8_t* __restrict__ mask, const float* __restrict__ s_loss,
+                      const float* __restrict__ s_ratio, const float* __restrict__ s_kl,
+                      const float* __restrict__ s_ent, const uint8_t* __restrict__ s_flags, SeqRec* recs) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * kSeqWarps + warp;
+  if (b >= B) return;
+  const int n = seq_len(lengths, b, T);
+  double loss = 0, ratio = 0, kl = 0, ent = 0, clipped = 0, dual = 0, tokens = 0, nfg = 0, nfl = 0;
+  for (int t = lane; t < n; t += 32) {
+    const int64_t i = (int64_t)b * T + t;
+    if (mask && !mask[i]) continue;
+    const uint8_t f = s_flags[i];
+    loss += (double)s_loss[i];
+    ratio += (double)s_ratio[i];
+    kl += (double)s_kl[i];
+    ent += (double)s_ent[i];
+    clipped += (f & TF_CLIPPED) ? 1.0 : 0.0;
+    dual += (f & TF_DUAL) ? 1.0 : 0.0;
+    nfg += (f & TF_NONFINITE_GRAD) ? 1.0 : 0.0;
+    nfl += (f & TF_NONFINITE_LOSS) ? 1.0 : 0.0;
+    tokens += 1.0;
+  }
+  loss = warp_sum(loss);
+  ratio = warp_sum(ratio);
+  kl = warp_sum(kl);
+  ent = warp_sum(ent);
+  clipped = warp_sum(clipped);
+  dual = warp_sum(dual);
+  tokens = warp_sum(tokens);
+  nfg = warp_sum(nfg);
+  nfl = warp_sum(nfl);
+  if (lane == 0) recs[seq_offset + b] = SeqRec{loss, ratio, kl, ent, clipped, dual, tokens, nfg, nfl, 0.0};
+}
+
+constexpr int kBR = 1024;
+constexpr int kNV = 13;
+
+__global__ void __launch_bounds__(kBR) batch_reduce_kernel(const SeqRec* __restrict__ recs, int nseq, int G,
+                                                           double* partials) {
+  __shared__ double sm[kNV][32];
+  double v[kNV];
+#pragma unroll
+  for (int k = 0; k < kNV; ++k) v[k] = 0.0;
+  for (int b = threadIdx.x; b < nseq; b += kBR) {
+    const SeqRec r = recs[b];
+    v[RLO_P_LOSS_SUM] += r.loss;
+    v[RLO_P_RATIO_SUM] += r.ratio;
+    v[RLO_P_KL_SUM] += r.kl;
+    v[RLO_P_ENTROPY_SUM] += r.entropy;
+    v[RLO_P_CLIPPED] += r.clipped;
+    v[RLO_P_DUAL_CLIPPED] += r.dual;
+    v[RLO_P_TOKENS] += r.tokens;
+    v[RLO_P_NONFINITE_GRAD] += r.nonfinite_grad;
+    v[RLO_P_NONFINITE_LOSS] += r.nonfinite_loss;
+    if (r.tokens > 0.0) {
+      v[RLO_P_SEQ_MEAN_SUM] += r.loss / r.tokens;
+      v[RLO_P_SEQS] += 1.0;
+    }
+  }
+  const int ngroups = (nseq + G - 1) / G;
+  for (int g = threadIdx.x; g < ngroups; g += kBR) {
+    double gl = 0.0, gt = 0.0;
+    const int e = min(nseq, (g + 1) * G);
+    for (int b = g * G; b < e; ++b) {
+      gl += recs[b].loss;
+      gt += recs[b].tokens;
+    }
+    if (gt > 0.0) {
+      v[RLO_P_GROUP_MEAN_SUM] += gl / gt;
+      v[RLO_P_GROUPS] += 1.0;
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < kNV; ++k) {
+    v[k] = warp_sum(v[k]);
+    if (lane == 0) sm[k][warp] = v[k];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < kNV; ++k) {
+      double x = sm[k][lane];
+      x = warp_sum(x);
+      if (lane == 0) partials[k] = x;
+    }
+    if (lane < RLO_NPARTIAL - kNV) partials[kNV + lane] = 0.0;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_seq_reduce(int32_t B, int32_t T, int32_t seq_offset, const int32_t* lengths,
+                              const uint8_t* mask, const float* s_loss, const float* s_ratio,
+                              const float* s_kl, const float* s_ent, const uint8_t* s_flags, SeqRec* recs,
+                              cudaStream_t s) {
+  if (B == 0) return cudaSuccess;
+  seq_reduce_kernel<<<(B + kSeqWarps - 1) / kSeqWarps, kSeqWarps * 32, 0, s>>>(
+      B, T, seq_offset, lengths, mask, s_loss, s_ratio, s_kl, s_ent, s_flags, recs);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_batch_reduce(const SeqRec* recs, int32_t nseq, int32_t G, double* partials, cudaStream_t s) {
+  batch_reduce_kernel<<<1, kBR, 0, s>>>(recs, nseq, G < 1 ? 1 : G, partials);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+}  // namespace rlo
