@@ -10,11 +10,13 @@
 //   compute_advantages         policy.cpp:257-311  -> rlo_compute_advantages
 //   ppo_gradient (loss part)   policy.cpp:313-374  -> rlo_ppo_gradient
 #include <cuda_runtime.h>
-#include <nccl.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: NCCL is bound at run time (see nccl_api())
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -46,10 +48,50 @@ rlo_status cuda_fail(cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #call);      \
   } while (0)
 
-#define RLO_NCCL(call)                                                                          \
-  do {                                                                                          \
-    ncclResult_t r_ = (call);                                                                   \
-    if (r_ != ncclSuccess) return fail(RLO_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+// NCCL is resolved with dlopen on first use instead of being linked: the
+// process may already hold a libnccl.so.2 (torch bundles NCCL 2.28 while the
+// system copy is 2.27), and two different copies of one SONAME in one process
+// break the one loaded second.  RTLD_NOLOAD picks the copy already resident;
+// RLO_NCCL_LIBRARY overrides; otherwise the default search path is used.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  std::string error;
+  bool ok() const { return GetUniqueId && CommInitRank && AllGather && CommDestroy && GetErrorString; }
+};
+
+const NcclApi& nccl_api() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) {
+      const char* env = std::getenv("RLO_NCCL_LIBRARY");
+      h = dlopen(env && *env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    }
+    if (!h) {
+      a.error = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return a;
+    }
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    if (!a.ok()) a.error = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+
+#define RLO_NCCL(call)                                                                                  \
+  do {                                                                                                  \
+    if (!nccl_api().ok()) return fail(RLO_ERR_NCCL, nccl_api().error);                                  \
+    ncclResult_t r_ = (call);                                                                           \
+    if (r_ != ncclSuccess)                                                                              \
+      return fail(RLO_ERR_NCCL, std::string(#call) + ": " + nccl_api().GetErrorString(r_));             \
   } while (0)
 
 #define RLO_TRY(call)                    \
@@ -271,7 +313,7 @@ rlo_status rlo_create(int32_t device, rlo_handle** out) {
 rlo_status rlo_destroy(rlo_handle* h) {
   if (!h) return RLO_OK;
   DeviceGuard g(h->device);
-  if (h->comm) ncclCommDestroy(h->comm);
+  if (h->comm && nccl_api().ok()) nccl_api().CommDestroy(h->comm);
   h->recs.release();
   h->s_loss.release();
   h->s_ratio.release();
@@ -303,7 +345,7 @@ rlo_status rlo_destroy(rlo_handle* h) {
 rlo_status rlo_comm_unique_id(void* id128) {
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
   ncclUniqueId id;
-  RLO_NCCL(ncclGetUniqueId(&id));
+  RLO_NCCL(nccl_api().GetUniqueId(&id));
   std::memcpy(id128, &id, sizeof(id));
   return RLO_OK;
 }
@@ -315,7 +357,7 @@ rlo_status rlo_comm_init(rlo_handle* h, const void* id128, int32_t rank, int32_t
   if (world > 1) {
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof(id));
-    RLO_NCCL(ncclCommInitRank(&h->comm, world, id, rank));
+    RLO_NCCL(nccl_api().CommInitRank(&h->comm, world, id, rank));
   }
   h->rank = rank;
   h->world = world;
@@ -453,7 +495,7 @@ rlo_status rlo_compute_advantages(rlo_handle* h, const rlo_train_config* cfg, co
     RLO_CUDA(launch_wstat_reduce(h->wstat.p, nslots, h->stats4.p, s));
     const double* stats = h->stats4.p;
     if (h->comm) {  // global whitening: all-gather (sum, sq, count), rank-ordered sum in the kernel
-      RLO_NCCL(ncclAllGather(h->stats4.p, h->stats_all.p, 4, ncclFloat64, h->comm, s));
+      RLO_NCCL(nccl_api().AllGather(h->stats4.p, h->stats_all.p, 4, ncclFloat64, h->comm, s));
       stats = h->stats_all.p;
     }
     RLO_CUDA(launch_whiten_clip(a, stats, h->comm ? h->world : 1, s));
@@ -567,7 +609,7 @@ rlo_status rlo_merge_gradients(rlo_handle* h, const rlo_train_config* cfg, rlo_s
   const int world = h->comm ? h->world : 1;
   if (h->comm) {
     // all-gather of the per-rank partials, merged below in rank order (policy.cpp:428-436)
-    RLO_NCCL(ncclAllGather(h->partials.p, h->gathered.p, RLO_NPARTIAL, ncclFloat64, h->comm, s));
+    RLO_NCCL(nccl_api().AllGather(h->partials.p, h->gathered.p, RLO_NPARTIAL, ncclFloat64, h->comm, s));
     RLO_CUDA(cudaMemcpyAsync(h->host_gathered, h->gathered.p, sizeof(double) * RLO_NPARTIAL * world,
                              cudaMemcpyDeviceToHost, s));
   } else {

@@ -86,7 +86,9 @@ template <>
 struct Vec<float> {
   using V = float4;
   static constexpr int kElems = 4;
-  __device__ static V fill() { return make_float4(kNegInit, kNegInit, kNegInit, kNegInit); }
+  // -inf padding: contributes exp2(-inf) = 0 and never raises the running max
+  // (a finite sentinel would leave a rounding residual ~ulp(1e30) in t).
+  __device__ static V fill() { return make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY); }
   template <int U>
   __device__ static float chunk_max(const V (&v)[U]) {
     float m = fmaxf(fmaxf(v[0].x, v[0].y), fmaxf(v[0].z, v[0].w));
@@ -115,7 +117,7 @@ template <>
 struct Vec<__nv_bfloat16> {
   using V = uint4;
   static constexpr int kElems = 8;
-  __device__ static V fill() { return make_uint4(0xF14AF14Au, 0xF14AF14Au, 0xF14AF14Au, 0xF14AF14Au); }
+  __device__ static V fill() { return make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u); }  // bf16 -inf
   __device__ static __nv_bfloat162 as_b2(uint32_t x) { return *reinterpret_cast<__nv_bfloat162*>(&x); }
   template <int U>
   __device__ static float chunk_max(const V (&v)[U]) {
