@@ -226,7 +226,8 @@ def run_ours(args, c):
         ms = float(tt.item())
 
     # ---- e2e: the reference-facing host-buffer call ------------------------
-    e2e = run_e2e(args, c, obj, rlo, torch, cfg, logits, side, dev, stream, dist, key_rows, mb)
+    e2e = None if args.no_e2e else run_e2e(args, c, obj, rlo, torch, cfg, logits, side, dev, stream, dist,
+                                           key_rows, mb)
 
     peak, peak_kind = load_peaks()
     tokens_per_step = B * T  # full-length responses, all positions loss-participating
@@ -424,6 +425,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-step-seconds", type=float, default=4.0)
     args = ap.parse_args()

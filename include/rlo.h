@@ -239,6 +239,13 @@ rlo_status rlo_ppo_gradient(rlo_handle* h, const rlo_train_config* cfg, const rl
 rlo_status rlo_merge_gradients(rlo_handle* h, const rlo_train_config* cfg, rlo_stats* out,
                                rlo_partials* out_partials, void* stream);
 
+/* The rank-local GradAccum scalars of everything accumulated since the last
+ * merge (what ppo_gradient returns per rank, policy.hpp:141): fixed-order
+ * reduction of the per-sequence records, no cross-rank exchange and no
+ * zero-token / non-finite checks (those belong to merge_gradients).
+ * Synchronises `stream`; resets the accumulator. */
+rlo_status rlo_rank_partials(rlo_handle* h, const rlo_train_config* cfg, rlo_partials* out, void* stream);
+
 /* The whole path for one step (compute_advantages -> ppo_gradient ->
  * merge_gradients) on device-resident inputs. */
 rlo_status rlo_objective_step(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch,

@@ -1,0 +1,147 @@
+// rlo.hpp — C++ surface over the C ABI (rlo.h), shaped like the reference's
+// include/rollmini/policy.hpp + errors.hpp so reference-side code can switch
+// with minimal edits:
+//
+//   rollmini::TrainConfig        -> rlo::TrainConfig      (policy.hpp:57-67, same defaults)
+//   rollmini::UpdateStats        -> rlo::UpdateStats      (policy.hpp:130-136, + extension stats)
+//   rollmini::InputError, ...    -> rlo::InputError, ...  (errors.hpp:11-82, same messages)
+//   compute_advantages / forward_logprobs / ppo_gradient / merge_gradients
+//                                -> rlo::Objective methods (one object per GPU per worker
+//                                   thread, like one PolicyWorkspace per worker)
+//   split_sizes                  -> rlo::split_sizes      (sample.hpp:51-53)
+//
+// Header-only; link with -lrlo (paper_2506_06122_b200/lib/librlo.so).
+// Streams are passed as void* (a cudaStream_t) so this header needs no CUDA
+// headers.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "rlo.h"
+
+namespace rlo {
+
+class Error : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class ConfigError : public Error {
+ public:
+  using Error::Error;
+};
+class InputError : public Error {
+ public:
+  using Error::Error;
+};
+class TrainingError : public Error {
+ public:
+  using Error::Error;
+};
+class DispatchError : public Error {
+ public:
+  using Error::Error;
+};
+class CollectError : public Error {
+ public:
+  using Error::Error;
+};
+class CudaError : public Error {
+ public:
+  using Error::Error;
+};
+
+inline void check(rlo_status s) {
+  if (s == RLO_OK) return;
+  const std::string msg = rlo_last_error();
+  switch (s) {
+    case RLO_ERR_INPUT: throw InputError(msg);
+    case RLO_ERR_CONFIG: throw ConfigError(msg);
+    case RLO_ERR_TRAINING: throw TrainingError(msg);
+    case RLO_ERR_NCCL: throw CollectError(msg);
+    case RLO_ERR_DISPATCH: throw DispatchError(msg);
+    case RLO_ERR_CUDA: throw CudaError(msg);
+    default: throw Error(msg);
+  }
+}
+
+struct TrainConfig : rlo_train_config {
+  TrainConfig() { rlo_train_config_default(this); }
+  void validate() const { check(rlo_train_config_validate(this)); }
+};
+
+using UpdateStats = rlo_stats;
+using Partials = rlo_partials;
+
+inline std::vector<int64_t> split_sizes(int64_t n, int32_t parts) {
+  std::vector<int64_t> out(static_cast<size_t>(parts > 0 ? parts : 0));
+  check(rlo_split_sizes(n, parts, out.data()));
+  return out;
+}
+
+inline std::pair<int32_t, int32_t> shard_plan(int32_t B, int32_t G, int32_t world, int32_t rank) {
+  int32_t b = 0, n = 0;
+  check(rlo_shard_plan(B, G, world, rank, &b, &n));
+  return {b, n};
+}
+
+inline UpdateStats merge_partials(const std::vector<Partials>& parts, const TrainConfig& cfg) {
+  UpdateStats st{};
+  check(rlo_merge_partials(parts.data(), static_cast<int32_t>(parts.size()), &cfg, &st));
+  return st;
+}
+
+// RAII owner of one rlo_handle (device workspace + optional NCCL group).
+class Objective {
+ public:
+  explicit Objective(int32_t device) { check(rlo_create(device, &h_)); }
+  ~Objective() { rlo_destroy(h_); }
+  Objective(const Objective&) = delete;
+  Objective& operator=(const Objective&) = delete;
+  Objective(Objective&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+
+  static std::vector<char> unique_id() {
+    std::vector<char> id(128);
+    check(rlo_comm_unique_id(id.data()));
+    return id;
+  }
+  void init_comm(const std::vector<char>& id, int32_t rank, int32_t world) {
+    check(rlo_comm_init(h_, id.data(), rank, world));
+  }
+
+  void forward_logprobs(const rlo_batch& batch, const rlo_logits& logits, float* logp, float* entropy = nullptr,
+                        float* token_logit = nullptr, void* stream = nullptr) {
+    check(rlo_forward_logprobs(h_, &batch, &logits, logp, entropy, token_logit, stream));
+  }
+  void compute_advantages(const TrainConfig& cfg, const rlo_batch& batch, const float* rewards_tok,
+                          const float* rewards_seq, const float* values, float* adv, float* returns = nullptr,
+                          void* stream = nullptr) {
+    check(rlo_compute_advantages(h_, &cfg, &batch, rewards_tok, rewards_seq, values, adv, returns, stream));
+  }
+  void ppo_gradient(const TrainConfig& cfg, const rlo_batch& batch, const rlo_logits& actor,
+                    const rlo_logits* old_logits, const rlo_logits* ref_logits, const float* old_logp,
+                    const float* ref_logp, const float* adv, const rlo_token_out* out = nullptr,
+                    void* stream = nullptr) {
+    check(rlo_ppo_gradient(h_, &cfg, &batch, &actor, old_logits, ref_logits, old_logp, ref_logp, adv, out, stream));
+  }
+  UpdateStats merge_gradients(const TrainConfig& cfg, Partials* mine = nullptr, void* stream = nullptr) {
+    UpdateStats st{};
+    check(rlo_merge_gradients(h_, &cfg, &st, mine, stream));
+    return st;
+  }
+  Partials rank_partials(const TrainConfig& cfg, void* stream = nullptr) {
+    Partials p{};
+    check(rlo_rank_partials(h_, &cfg, &p, stream));
+    return p;
+  }
+  void sync(void* stream = nullptr) { check(rlo_sync(h_, stream)); }
+  rlo_handle* get() const { return h_; }
+
+ private:
+  rlo_handle* h_ = nullptr;
+};
+
+}  // namespace rlo

@@ -99,6 +99,7 @@ def lib() -> C.CDLL:
         "rlo_ppo_gradient": ([vp, P(rlo_train_config), P(rlo_batch), P(rlo_logits), P(rlo_logits),
                               P(rlo_logits), vp, vp, vp, P(rlo_token_out), vp], C.c_int),
         "rlo_merge_gradients": ([vp, P(rlo_train_config), P(rlo_stats), P(rlo_partials), vp], C.c_int),
+        "rlo_rank_partials": ([vp, P(rlo_train_config), P(rlo_partials), vp], C.c_int),
         "rlo_objective_step": ([vp, P(rlo_train_config), P(rlo_batch), vp, vp, vp, P(rlo_logits), P(rlo_logits),
                                 P(rlo_logits), vp, vp, vp, P(rlo_token_out), P(rlo_stats), vp], C.c_int),
         "rlo_objective_step_host": ([vp, P(rlo_train_config), i32, i32, vp, vp, vp, vp, vp, vp, P(rlo_logits),

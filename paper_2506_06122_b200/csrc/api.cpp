@@ -628,6 +628,28 @@ rlo_status rlo_merge_gradients(rlo_handle* h, const rlo_train_config* cfg, rlo_s
   return rlo_merge_partials(parts.data(), world, cfg, out);
 }
 
+rlo_status rlo_rank_partials(rlo_handle* h, const rlo_train_config* cfg, rlo_partials* out, void* stream) {
+  if (!h) return fail(RLO_ERR_INPUT, "rank_partials: null handle");
+  RLO_TRY(rlo_train_config_validate(cfg));
+  DeviceGuard g(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int32_t nseq = h->acc_nseq;
+  if (nseq > 0) {
+    RLO_CUDA(launch_batch_reduce(h->recs.p, nseq, cfg->group_size, h->partials.p, s));
+  } else {
+    RLO_CUDA(cudaMemsetAsync(h->partials.p, 0, sizeof(double) * RLO_NPARTIAL, s));
+  }
+  RLO_CUDA(cudaMemcpyAsync(h->host_gathered, h->partials.p, sizeof(double) * RLO_NPARTIAL, cudaMemcpyDeviceToHost, s));
+  RLO_CUDA(cudaMemcpyAsync(h->host_err, h->err.p, sizeof(DevError), cudaMemcpyDeviceToHost, s));
+  RLO_CUDA(cudaMemsetAsync(h->err.p, 0, sizeof(DevError), s));
+  if (nseq > 0) RLO_CUDA(cudaMemsetAsync(h->recs.p, 0, sizeof(SeqRec) * static_cast<size_t>(nseq), s));
+  h->acc_nseq = 0;
+  RLO_CUDA(cudaStreamSynchronize(s));
+  RLO_TRY(collect_device_error(h, s));
+  if (out) std::memcpy(out->v, h->host_gathered, sizeof(double) * RLO_NPARTIAL);
+  return RLO_OK;
+}
+
 rlo_status rlo_objective_step(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch,
                               const float* rewards_tok, const float* rewards_seq, const float* values,
                               const rlo_logits* actor_logits, const rlo_logits* old_logits,

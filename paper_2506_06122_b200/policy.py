@@ -292,6 +292,13 @@ class Objective:
         stats = UpdateStats.from_c(st)
         return (stats, np.array(part.v[:])) if with_partials else stats
 
+    def rank_partials(self, cfg: TrainConfig, stream=None) -> np.ndarray:
+        """This rank's GradAccum scalars (no cross-rank merge, no checks); resets."""
+        part = _abi.rlo_partials()
+        check(_abi.lib().rlo_rank_partials(self._h, C.byref(cfg.to_c()), C.byref(part),
+                                           _stream(stream, self.device)))
+        return np.array(part.v[:])
+
     def step(self, cfg: TrainConfig, tokens, lengths, actor_logits, mask=None, rewards=None, scalar_rewards=None,
              values=None, old_logits=None, ref_logits=None, old_logprobs=None, ref_logprobs=None, adv_out=None,
              stream=None) -> UpdateStats:
@@ -381,7 +388,7 @@ class PolicyWorker:
             self.obj.ppo_gradient(self.train_config, b["response_tokens"], b["lengths"], b["logits"],
                                   b["advantages"], mask=b.get("action_mask"), old_logprobs=b["response_logprobs"],
                                   ref_logprobs=b.get("ref_logprobs"), outputs=("dlogp",))
-            stats, p = self.obj.merge_gradients(self.train_config, with_partials=True)
+            p = self.obj.rank_partials(self.train_config)
             out = Message()
             out.scalars = {"loss_sum": p[0], "ratio_sum": p[1], "kl_sum": p[2], "clipped": p[4], "tokens": p[6]}
             return out
