@@ -179,6 +179,13 @@ rlo_status rlo_shard_plan(int32_t B, int32_t G, int32_t world, int32_t rank,
 rlo_status rlo_merge_partials(const rlo_partials* parts, int32_t nranks,
                               const rlo_train_config* cfg, rlo_stats* out);
 
+/* Whitening parameters (policy.cpp:288-302) from rank-ordered statistics
+ * stats_all[r*4 + {0,1,2}] = (sum, sum of squares, count) over masked
+ * positions of rank r: mean, inv = 1/(sqrt(max(0, E[x^2]-mean^2)) + 1e-8).
+ * Returns 1 when whitening applies (count > 0), else 0.  The device
+ * normalise pass runs this same code on the all-gathered statistics. */
+int32_t rlo_whiten_combine(const double* stats_all, int32_t world, double* mean, double* inv);
+
 /* ---- handle ------------------------------------------------------------ */
 rlo_status rlo_create(int32_t device, rlo_handle** out);
 rlo_status rlo_destroy(rlo_handle* h);

@@ -90,6 +90,7 @@ def lib() -> C.CDLL:
         "rlo_split_sizes": ([i64, i32, P(i64)], C.c_int),
         "rlo_shard_plan": ([i32, i32, i32, i32, P(i32), P(i32)], C.c_int),
         "rlo_merge_partials": ([P(rlo_partials), i32, P(rlo_train_config), P(rlo_stats)], C.c_int),
+        "rlo_whiten_combine": ([vp, i32, P(C.c_double), P(C.c_double)], C.c_int32),
         "rlo_create": ([i32, P(vp)], C.c_int),
         "rlo_destroy": ([vp], C.c_int),
         "rlo_comm_unique_id": ([vp], C.c_int),

@@ -114,7 +114,8 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const AdvArgs a) {
     const int64_t i = (int64_t)b * a.T + t;
     if (a.out_returns) a.out_returns[i] = (float)(gae ? acc + (double)vv[t] : acc);
     if (a.whiten) {
-      a.out_adv[i] = (float)acc;  // raw; normalised + clipped by whiten_clip_kernel
+      a.raw64[i] = acc;  // raw fp64; normalised + clipped by whiten_clip_kernel (fp32 storage would
+                         // amplify rounding by 1/std when the masked variance is tiny)
       if (!a.mask || a.mask[i]) {
         ssum += acc;
         ssq += acc * acc;
@@ -177,6 +178,7 @@ __global__ void __launch_bounds__(kScanThreads) grpo_kernel(const AdvArgs a) {
       const int64_t i = (int64_t)b * a.T + t;
       const bool valid = t < n;
       a.out_adv[i] = valid ? outv : 0.f;
+      if (a.whiten) a.raw64[i] = valid ? adv : 0.0;
       if (a.out_returns) a.out_returns[i] = valid ? (float)R[k] : 0.f;
       if (a.whiten && valid && (!a.mask || a.mask[i])) {
         ssum += adv;
@@ -214,26 +216,17 @@ __global__ void whiten_clip_kernel(const AdvArgs a, const double* __restrict__ s
   __shared__ double s_mean, s_inv;
   __shared__ int s_apply;
   if (threadIdx.x == 0) {
-    double sum = 0.0, sq = 0.0, cnt = 0.0;
-    for (int r = 0; r < world; ++r) {
-      sum += stats_all[r * 4 + 0];
-      sq += stats_all[r * 4 + 1];
-      cnt += stats_all[r * 4 + 2];
-    }
-    s_apply = cnt > 0.0;
-    if (cnt > 0.0) {
-      const double mean = sum / cnt;
-      const double var = fmax(0.0, sq / cnt - mean * mean);
-      s_mean = mean;
-      s_inv = 1.0 / (sqrt(var) + 1e-8);
-    }
+    double mean = 0.0, inv = 1.0;
+    s_apply = whiten_combine(stats_all, world, &mean, &inv);
+    s_mean = mean;
+    s_inv = inv;
   }
   __syncthreads();
   const int64_t N = (int64_t)a.B * a.T;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
     const int b = (int)(i / a.T), t = (int)(i - (int64_t)b * a.T);
     if (t >= seq_len(a.lengths, b, a.T)) continue;
-    double v = (double)a.out_adv[i];
+    double v = a.raw64[i];
     if (s_apply) v = (v - s_mean) * s_inv;
     a.out_adv[i] = (float)clampd(v, -a.adv_clip, a.adv_clip);
   }

@@ -151,6 +151,7 @@ struct rlo_handle {
   DevBuf<uint8_t> s_flags;
   // whitening
   DevBuf<WStat> wstat;
+  DevBuf<double> raw64;
   DevBuf<double> stats4, stats_all, partials, gathered;
   DevBuf<DevError> err;
   // staging for rlo_objective_step_host and internal advantages
@@ -278,6 +279,11 @@ rlo_status rlo_merge_partials(const rlo_partials* parts, int32_t nranks, const r
   return RLO_OK;
 }
 
+int32_t rlo_whiten_combine(const double* stats_all, int32_t world, double* mean, double* inv) {
+  if (!stats_all || world <= 0 || !mean || !inv) return 0;
+  return whiten_combine(stats_all, world, mean, inv);
+}
+
 // ---------------------------------------------------------------------------
 // handle
 // ---------------------------------------------------------------------------
@@ -321,6 +327,7 @@ rlo_status rlo_destroy(rlo_handle* h) {
   h->s_ent.release();
   h->s_flags.release();
   h->wstat.release();
+  h->raw64.release();
   h->stats4.release();
   h->stats_all.release();
   h->partials.release();
@@ -489,6 +496,8 @@ rlo_status rlo_compute_advantages(rlo_handle* h, const rlo_train_config* cfg, co
   if (a.whiten) {
     RLO_CUDA(h->wstat.ensure(static_cast<size_t>(nslots)));
     a.wstat = h->wstat.p;
+    RLO_CUDA(h->raw64.ensure(static_cast<size_t>((int64_t)B * T)));
+    a.raw64 = h->raw64.p;
   }
   RLO_CUDA(launch_advantages(a, s));
   if (a.whiten) {

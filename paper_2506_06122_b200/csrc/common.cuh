@@ -32,6 +32,53 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   return r;
 }
 
+// ---- packed fp32x2 (sm_100 FFMA2 / FADD2: two fp32 lanes per instruction) ----
+using f2 = unsigned long long;
+__device__ __forceinline__ f2 pk2(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk2(f2 v, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
+__device__ __forceinline__ f2 ffma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2 fadd2(f2 a, f2 b) {
+  f2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// 2^t for a pair on the FMA pipe (FA4-style MUFU offload): Cody-Waite split
+// t = j + f, j = rint(t) via the 1.5*2^23 magic add, f in [-0.5, 0.5];
+// degree-5 polynomial (relative error 1.9e-7 in fp32 Horner, on par with
+// MUFU.EX2's ~2 ulp); 2^j inserted into the exponent with one IMAD.
+// Inputs are clamped to >= -126 so the exponent add stays in the normal
+// range: t <= -126 yields 2^-126 (1.2e-38) instead of 0, which is below the
+// fp32 resolution of any sum it enters (s >= 1: it contains the max term).
+__device__ __forceinline__ f2 exp2_poly2(float tl, float th) {
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+  tl = fmaxf(tl, -126.0f);
+  th = fmaxf(th, -126.0f);
+  const f2 t = pk2(tl, th);
+  const f2 r = fadd2(t, pk2(kMagic, kMagic));
+  const f2 j = fadd2(r, pk2(-kMagic, -kMagic));
+  const f2 f = ffma2(j, pk2(-1.0f, -1.0f), t);
+  f2 p = ffma2(f, pk2(0x1.5bba14p-10f, 0x1.5bba14p-10f), pk2(0x1.3cea88p-7f, 0x1.3cea88p-7f));
+  p = ffma2(p, f, pk2(0x1.c6b752p-5f, 0x1.c6b752p-5f));
+  p = ffma2(p, f, pk2(0x1.ebf9bcp-3f, 0x1.ebf9bcp-3f));
+  p = ffma2(p, f, pk2(0x1.62e42ap-1f, 0x1.62e42ap-1f));
+  p = ffma2(p, f, pk2(1.0f, 1.0f));
+  float pl, ph, rl, rh;
+  upk2(p, pl, ph);
+  upk2(r, rl, rh);
+  const uint32_t bl = __float_as_uint(rl) * 8388608u + __float_as_uint(pl);  // + (j << 23)
+  const uint32_t bh = __float_as_uint(rh) * 8388608u + __float_as_uint(ph);
+  return pk2(__uint_as_float(bl), __uint_as_float(bh));
+}
+
 __device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 

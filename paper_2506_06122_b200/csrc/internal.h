@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cmath>
 
 #include "../../include/rlo.h"
 
@@ -37,6 +38,32 @@ struct SeqRec {
 struct WStat {
   double sum, sq, count, pad;
 };
+
+#if defined(__CUDACC__)
+#define RLO_HOST_DEVICE __host__ __device__
+#else
+#define RLO_HOST_DEVICE
+#endif
+
+// Whitening parameters from rank-ordered statistics stats_all[r*4 + {0,1,2}] =
+// (sum, sum of squares, count) over masked positions (policy.cpp:288-302):
+// mean, var = max(0, E[x^2] - mean^2), inv = 1/(sqrt(var) + 1e-8).  Returns 0
+// (no whitening) when the count is zero.  Shared by whiten_clip_kernel and the
+// host (rlo_whiten_combine), so the CPU multi-rank tests exercise this code.
+RLO_HOST_DEVICE inline int whiten_combine(const double* stats_all, int world, double* mean, double* inv) {
+  double sum = 0.0, sq = 0.0, cnt = 0.0;
+  for (int r = 0; r < world; ++r) {
+    sum += stats_all[r * 4 + 0];
+    sq += stats_all[r * 4 + 1];
+    cnt += stats_all[r * 4 + 2];
+  }
+  if (!(cnt > 0.0)) return 0;
+  const double m = sum / cnt;
+  const double d = sq / cnt - m * m;
+  *mean = m;
+  *inv = 1.0 / (sqrt(d > 0.0 ? d : 0.0) + 1e-8);
+  return 1;
+}
 
 struct VocabArgs {
   const void* logits[3];
@@ -89,7 +116,8 @@ struct AdvArgs {
   int32_t whiten;
   int32_t G, ddof;
   double grpo_eps;
-  WStat* wstat;  // [B] (scan) or [B/G] (GRPO) when whiten
+  WStat* wstat;   // [B] (scan) or [B/G] (GRPO) when whiten
+  double* raw64;  // [B*T] raw advantages in fp64 when whiten
 };
 
 // Launchers (return cudaGetLastError()).

@@ -1,0 +1,375 @@
+// vocab_common.cuh — the online log-sum-exp state, per-dtype chunk math and
+// the per-row epilogue shared by the two vocab-pass kernels (vocab.cu: 128-bit
+// LDG streaming; vocab_tma.cu: TMA bulk-copy shared-memory ring).
+//
+// State per (thread, tensor), in log2 units relative to the fp32 constant kL2E:
+//   mL = running max of z*kL2E (fp32-rounded), s = sum 2^(z*kL2E - mL),
+//   w  = sum 2^(z*kL2E - mL) * (z*kL2E - mL)   (entropy; actor row only).
+// Per element: one FFMA (t = z*kL2E - mL), one MUFU.EX2, one FADD (+ one FFMA
+// for w).  The chunk max is taken first so the rescale (one more EX2) happens
+// only when a chunk raises the max.  finish() returns to natural units in
+// fp64: lse = (mL + log2 s) / kL2E, H = (log2 s - w/s) / kL2E.
+#pragma once
+
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace rlo {
+namespace vocab {
+
+struct Acc {
+  float mL;
+  float s;
+  float w;
+};
+
+__device__ __forceinline__ void acc_init(Acc& a) {
+  a.mL = kNegInit * kL2E;
+  a.s = 0.f;
+  a.w = 0.f;
+}
+
+template <bool ENT>
+__device__ __forceinline__ void acc_rescale(Acc& a, float newmL) {
+  if (newmL > a.mL) {
+    const float d = a.mL - newmL;
+    const float sc = ex2(d);
+    if (ENT) a.w = (a.w + a.s * d) * sc;
+    a.s *= sc;
+    a.mL = newmL;
+  }
+}
+
+template <bool ENT>
+__device__ __forceinline__ void acc_elem(float z, float mL, float& s, float& w) {
+  const float t = fmaf(z, kL2E, -mL);
+  const float e = ex2(t);
+  s += e;
+  if (ENT) w = fmaf(e, fmaxf(t, kNegInit), w);  // guard: -inf logits give e = 0, not 0 * -inf
+}
+
+template <bool ENT>
+__device__ __forceinline__ void acc_combine(Acc& a, float mL2, float s2, float w2) {
+  const float M = fmaxf(a.mL, mL2);
+  const float d1 = a.mL - M, d2 = mL2 - M;
+  const float e1 = ex2(d1), e2 = ex2(d2);
+  if (ENT) a.w = (a.w + a.s * d1) * e1 + (w2 + s2 * d2) * e2;
+  a.s = a.s * e1 + s2 * e2;
+  a.mL = M;
+}
+
+template <bool ENT>
+__device__ __forceinline__ void acc_warp_reduce(Acc& a) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, a.mL, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, a.s, o);
+    const float w2 = ENT ? __shfl_xor_sync(0xffffffffu, a.w, o) : 0.f;
+    acc_combine<ENT>(a, m2, s2, w2);
+  }
+}
+
+// ---- per-dtype 16-byte vector math -------------------------------------------
+//
+// MATH selects the per-element instruction mix (runtime-selected, see
+// vocab.cu: RLO_VOCAB_MATH; defaults per dtype):
+//   0  scalar FFMA / MUFU.EX2 / FADD per element;
+//   1  packed: FFMA2 / FADD2 on element pairs, MUFU.EX2 per element;
+//   2  as 1, plus 1 of 4 element pairs of each non-entropy row through the
+//      FMA-pipe polynomial exp2 (exp2_poly2) instead of MUFU (25% offload);
+//   3  as 2 with 2 of 4 pairs (50% offload).
+// The entropy (actor) row always uses MUFU: its 2^-126 floor would leak
+// into the entropy accumulator w.
+
+template <bool ENT>
+__device__ __forceinline__ void pair2(float zl, float zh, f2 L2, f2 nmL, f2& s, f2& w, bool poly) {
+  const f2 t = ffma2(pk2(zl, zh), L2, nmL);
+  float tl, th;
+  upk2(t, tl, th);
+  const f2 e = poly ? exp2_poly2(tl, th) : pk2(ex2(tl), ex2(th));
+  s = fadd2(s, e);
+  if (ENT) w = ffma2(e, pk2(fmaxf(tl, kNegInit), fmaxf(th, kNegInit)), w);
+}
+
+__device__ __forceinline__ float hsum2(f2 a, f2 b) {
+  float l, h;
+  upk2(fadd2(a, b), l, h);
+  return l + h;
+}
+
+template <typename ET>
+struct Vec;
+
+template <>
+struct Vec<float> {
+  using V = float4;
+  static constexpr int kElems = 4;
+  // -inf padding contributes exp2(-inf) = 0 and never raises the running max.
+  __device__ static V fill() { return make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY); }
+  template <int U>
+  __device__ static float chunk_max(const V (&v)[U]) {
+    float m = fmaxf(fmaxf(v[0].x, v[0].y), fmaxf(v[0].z, v[0].w));
+#pragma unroll
+    for (int u = 1; u < U; ++u) m = fmaxf(m, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
+    return m;
+  }
+  template <int U, bool ENT, int MATH>
+  __device__ static void accumulate(const V (&v)[U], Acc& a) {
+    acc_rescale<ENT>(a, chunk_max<U>(v) * kL2E);
+    if (MATH == 0) {
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, w0 = 0.f, w1 = 0.f, w2 = 0.f, w3 = 0.f;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        acc_elem<ENT>(v[u].x, a.mL, s0, w0);
+        acc_elem<ENT>(v[u].y, a.mL, s1, w1);
+        acc_elem<ENT>(v[u].z, a.mL, s2, w2);
+        acc_elem<ENT>(v[u].w, a.mL, s3, w3);
+      }
+      a.s += (s0 + s1) + (s2 + s3);
+      if (ENT) a.w += (w0 + w1) + (w2 + w3);
+    } else {
+      const f2 L2 = pk2(kL2E, kL2E), nmL = pk2(-a.mL, -a.mL);
+      f2 s0 = 0, s1 = 0, w0 = 0, w1 = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        pair2<ENT>(v[u].x, v[u].y, L2, nmL, s0, w0, false);
+        pair2<ENT>(v[u].z, v[u].w, L2, nmL, s1, w1, !ENT && MATH >= 2 && (u & 1));
+      }
+      a.s += hsum2(s0, s1);
+      if (ENT) a.w += hsum2(w0, w1);
+    }
+  }
+  __device__ static float scalar(const float* p) { return __ldg(p); }
+};
+
+template <>
+struct Vec<__nv_bfloat16> {
+  using V = uint4;
+  static constexpr int kElems = 8;
+  __device__ static V fill() { return make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u); }  // -inf
+  __device__ static __nv_bfloat162 as_b2(uint32_t x) { return *reinterpret_cast<__nv_bfloat162*>(&x); }
+  template <int U>
+  __device__ static float chunk_max(const V (&v)[U]) {
+    __nv_bfloat162 m = __hmax2(__hmax2(as_b2(v[0].x), as_b2(v[0].y)), __hmax2(as_b2(v[0].z), as_b2(v[0].w)));
+#pragma unroll
+    for (int u = 1; u < U; ++u)
+      m = __hmax2(m, __hmax2(__hmax2(as_b2(v[u].x), as_b2(v[u].y)), __hmax2(as_b2(v[u].z), as_b2(v[u].w))));
+    return fmaxf(__low2float(m), __high2float(m));
+  }
+  template <bool ENT>
+  __device__ static void word(uint32_t x, float mL, float& s0, float& s1, float& w0, float& w1) {
+    acc_elem<ENT>(bf16lo(x), mL, s0, w0);
+    acc_elem<ENT>(bf16hi(x), mL, s1, w1);
+  }
+  template <int U, bool ENT, int MATH>
+  __device__ static void accumulate(const V (&v)[U], Acc& a) {
+    acc_rescale<ENT>(a, chunk_max<U>(v) * kL2E);
+    if (MATH == 0) {
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, w0 = 0.f, w1 = 0.f, w2 = 0.f, w3 = 0.f;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        word<ENT>(v[u].x, a.mL, s0, s1, w0, w1);
+        word<ENT>(v[u].y, a.mL, s2, s3, w2, w3);
+        word<ENT>(v[u].z, a.mL, s0, s1, w0, w1);
+        word<ENT>(v[u].w, a.mL, s2, s3, w2, w3);
+      }
+      a.s += (s0 + s1) + (s2 + s3);
+      if (ENT) a.w += (w0 + w1) + (w2 + w3);
+    } else {
+      const f2 L2 = pk2(kL2E, kL2E), nmL = pk2(-a.mL, -a.mL);
+      f2 s0 = 0, s1 = 0, w0 = 0, w1 = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        pair2<ENT>(bf16lo(v[u].x), bf16hi(v[u].x), L2, nmL, s0, w0, false);
+        pair2<ENT>(bf16lo(v[u].y), bf16hi(v[u].y), L2, nmL, s1, w1, !ENT && MATH >= 2);
+        pair2<ENT>(bf16lo(v[u].z), bf16hi(v[u].z), L2, nmL, s0, w0, false);
+        pair2<ENT>(bf16lo(v[u].w), bf16hi(v[u].w), L2, nmL, s1, w1, !ENT && MATH >= 3);
+      }
+      a.s += hsum2(s0, s1);
+      if (ENT) a.w += hsum2(w0, w1);
+    }
+  }
+  __device__ static float scalar(const __nv_bfloat16* p) {
+    return __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(p)));
+  }
+};
+
+template <typename ET>
+__device__ __forceinline__ float load_logit(const void* base, int64_t off) {
+  return Vec<ET>::scalar(reinterpret_cast<const ET*>(base) + off);
+}
+
+struct RowResult {
+  double lse;
+  double entropy;
+};
+
+__device__ __forceinline__ RowResult finish(const Acc& a) {
+  const double l2 = log2((double)a.s);
+  RowResult r;
+  r.lse = ((double)a.mL + l2) / (double)kL2E;
+  r.entropy = (l2 - (double)a.w / (double)a.s) / (double)kL2E;
+  return r;
+}
+
+__device__ __forceinline__ void flag_error(const VocabArgs& a, int code, int value) {
+  if (atomicCAS(&a.err->code, 0, code) == 0) a.err->value = value;
+}
+
+// Loss epilogue for one loss-participating token (policy.cpp:355-374 + extensions), fp64.
+__device__ inline void loss_epilogue(const VocabArgs& a, int64_t row, double lp, double old, bool has_ref, double ref,
+                                     double ent) {
+  const double A = (double)a.adv[row];
+  const double eps = a.clip_eps;
+  const double ratio = exp(lp - old);                       // policy.cpp:358
+  const double rcl = clampd(ratio, 1.0 - eps, 1.0 + eps);  // :359
+  const double u = ratio * A, c = rcl * A;                  // :360-361
+  const double surr = (c < u) ? c : u;                      // :362 std::min
+  double pg = -surr;
+  bool dual = false;
+  if (a.dual_c > 1.0 && A < 0.0) {  // dual-clip: cap the A<0 loss at -c*A
+    const double cap = -a.dual_c * A;
+    if (pg > cap) {
+      pg = cap;
+      dual = true;
+    }
+  }
+  double k = 0.0, dk = 0.0;
+  if (has_ref) {
+    const double r = lp - ref;
+    if (a.kl_est == RLO_KL_K2) {
+      k = 0.5 * r * r;
+      dk = r;
+    } else if (a.kl_est == RLO_KL_K3) {
+      const double er = exp(-r);
+      k = er - 1.0 + r;
+      dk = 1.0 - er;
+    } else {
+      k = r;
+      dk = 1.0;
+    }
+  }
+  const double kc = a.kl_coef;
+  const double loss = pg + kc * (kc > 0.0 ? k : 0.0);                   // :364-366
+  const bool flows = A >= 0.0 ? ratio <= 1.0 + eps : ratio >= 1.0 - eps;  // :373
+  double dlp = (flows && !dual) ? -ratio * A : 0.0;                      // :374
+  dlp += kc > 0.0 ? kc * dk : 0.0;
+  uint8_t flags = 0;
+  if (u > c) flags |= TF_CLIPPED;  // :369
+  if (dual) flags |= TF_DUAL;
+  if (!isfinite(dlp)) flags |= TF_NONFINITE_GRAD;
+  if (!isfinite(loss)) flags |= TF_NONFINITE_LOSS;
+  a.s_loss[row] = (float)loss;
+  a.s_ratio[row] = (float)ratio;
+  a.s_kl[row] = has_ref ? (float)k : 0.f;
+  a.s_ent[row] = (float)ent;
+  a.s_flags[row] = flags;
+  if (a.o_logp) a.o_logp[row] = (float)lp;
+  if (a.o_old) a.o_old[row] = (float)old;
+  if (a.o_ref) a.o_ref[row] = has_ref ? (float)ref : 0.f;
+  if (a.o_ent) a.o_ent[row] = (float)ent;
+  if (a.o_dlogp) a.o_dlogp[row] = (float)dlp;
+  if (a.o_loss) a.o_loss[row] = (float)loss;
+}
+
+// Is `row` processed by this pass?  (forward_logprobs: every valid position;
+// loss: valid and mask != 0, policy.cpp:348-351.)  Also reports bad lengths.
+template <bool LOSS>
+__device__ __forceinline__ bool row_active(const VocabArgs& a, int64_t row, bool report) {
+  const int b = (int)(row / a.T);
+  const int t = (int)(row - (int64_t)b * a.T);
+  if (report && t == 0) {
+    const int raw = __ldg(a.lengths + b);
+    if (raw < 0 || raw > a.T) flag_error(a, DE_BAD_LENGTH, b);
+  }
+  bool active = t < seq_len(a.lengths, b, a.T);
+  if (LOSS && active && a.mask) active = __ldg(a.mask + row) != 0;
+  return active;
+}
+
+template <bool LOSS>
+__device__ __forceinline__ void write_inactive(const VocabArgs& a, int64_t row) {
+  if (!LOSS) {
+    a.out_lp[row] = 0.f;
+    if (a.out_ent) a.out_ent[row] = 0.f;
+    if (a.out_tok) a.out_tok[row] = 0.f;
+  } else {
+    if (a.o_logp) a.o_logp[row] = 0.f;
+    if (a.o_old) a.o_old[row] = 0.f;
+    if (a.o_ref) a.o_ref[row] = 0.f;
+    if (a.o_ent) a.o_ent[row] = 0.f;
+    if (a.o_dlogp) a.o_dlogp[row] = 0.f;
+    if (a.o_loss) a.o_loss[row] = 0.f;
+  }
+}
+
+// Token gather for the row (one thread): bit-exact element loads.
+template <typename ET, int NT>
+__device__ __forceinline__ void gather_token(const VocabArgs& a, int64_t row, int& tok, bool& oov, float (&ztok)[NT]) {
+  tok = __ldg(a.tokens + row);
+  oov = tok < 0 || tok >= a.V;
+#pragma unroll
+  for (int k = 0; k < NT; ++k) ztok[k] = oov ? 0.f : load_logit<ET>(a.logits[k], row * a.stride[k] + tok);
+}
+
+// Final cross-warp combine + outputs, executed by one full warp (all lanes):
+// red[w][k][0..2] holds warp w's (mL, s, w) for tensor k.
+template <int NT, int NWARPS, bool LOSS, bool ENT0>
+__device__ __forceinline__ void row_finish(const VocabArgs& a, const float (*red)[NT][3], int64_t row, int tok,
+                                           bool oov, const float (&ztok)[NT], int lane) {
+  double lse[NT], ent = 0.0;
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    Acc c;
+    if (lane < NWARPS) {
+      c.mL = red[lane][k][0];
+      c.s = red[lane][k][1];
+      c.w = red[lane][k][2];
+    } else {
+      acc_init(c);
+    }
+    if (k == 0 && ENT0)
+      acc_warp_reduce<true>(c);
+    else
+      acc_warp_reduce<false>(c);
+    const RowResult r = finish(c);
+    lse[k] = r.lse;
+    if (k == 0) ent = r.entropy;
+  }
+  if (lane != 0) return;
+  if (oov) flag_error(a, LOSS ? DE_OOV_LOSS : DE_OOV_LOGPROB, tok);
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+  double lp[NT];
+#pragma unroll
+  for (int k = 0; k < NT; ++k) lp[k] = oov ? nan : (double)ztok[k] - lse[k];  // policy.cpp:122, :227
+  if (!LOSS) {
+    a.out_lp[row] = (float)lp[0];
+    if (a.out_ent) a.out_ent[row] = (float)ent;
+    if (a.out_tok) a.out_tok[row] = ztok[0];
+    return;
+  }
+  double old = 0.0, ref = 0.0;
+  bool have_old = false, have_ref = false;
+#pragma unroll
+  for (int k = 1; k < NT; ++k) {
+    if (a.role[k] == ROLE_OLD) {
+      old = lp[k];
+      have_old = true;
+    }
+    if (a.role[k] == ROLE_REF) {
+      ref = lp[k];
+      have_ref = true;
+    }
+  }
+  if (!have_old) old = (double)a.old_lp_in[row];
+  if (!have_ref && a.ref_lp_in) {
+    ref = (double)a.ref_lp_in[row];
+    have_ref = true;
+  }
+  loss_epilogue(a, row, lp[0], old, have_ref, ref, ent);
+}
+
+}  // namespace vocab
+}  // namespace rlo

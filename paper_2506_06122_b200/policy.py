@@ -115,6 +115,14 @@ def merge_partials(parts: np.ndarray, cfg: TrainConfig) -> UpdateStats:
     return UpdateStats.from_c(st)
 
 
+def whiten_combine(stats_all: np.ndarray):
+    """(apply, mean, inv) from rank-ordered [world, 4] whitening statistics."""
+    st = np.ascontiguousarray(np.atleast_2d(stats_all), dtype=np.float64)
+    m, i = C.c_double(), C.c_double()
+    ok = _abi.lib().rlo_whiten_combine(st.ctypes.data_as(C.c_void_p), st.shape[0], C.byref(m), C.byref(i))
+    return bool(ok), m.value, i.value
+
+
 def launch_count() -> int:
     return int(_abi.lib().rlo_launch_count())
 

@@ -1,0 +1,232 @@
+// integration_main.cpp — drop-in check at the reference's own API level.
+//
+// Runs the reference's PolicyWorker (policy_workers.cpp, compiled from
+// /root/reference into oracle/_ref) and the B200PolicyWorker
+// (integration/b200_policy_worker.cpp -> librlo.so) on the same Messages and
+// compares their replies, then drives B200 workers through the reference's
+// own Cluster + cluster_forward_logprobs (cluster.cpp, policy_workers.cpp:298-303).
+// Both see identical logits: the reference through the "b2 trick"
+// (PolicyLayout{V,1,1,1}, all parameters 0 except b2 := row, so every
+// position's logits equal `row`), the B200 worker through a LogitsProvider
+// that tiles the same row into device memory.
+//
+// Exit code 0 = all checks passed.  Built by tests/cpp/Makefile (needs the
+// reference headers); run by tests/test_gpu_integration.py on a B200.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "b200_policy_worker.hpp"
+#include "rollmini/cluster.hpp"
+#include "rollmini/errors.hpp"
+#include "rollmini/policy.hpp"
+#include "rollmini/policy_workers.hpp"
+#include "rollmini/rng.hpp"
+#include "rollmini/vocab.hpp"
+
+using namespace rollmini;
+
+namespace {
+
+int g_fail = 0;
+
+void check(bool ok, const std::string& what) {
+  std::printf("%s %s\n", ok ? "PASS" : "FAIL", what.c_str());
+  if (!ok) ++g_fail;
+}
+
+bool close(double g, double r, double tol = 1e-5) { return std::fabs(g - r) <= tol * std::max(1.0, std::fabs(r)); }
+
+// Device logits provider: every row of the padded view equals `row`.
+struct TiledRow {
+  std::vector<float> row;
+  float* dev = nullptr;
+  size_t cap = 0;
+  rlo_logits operator()(const SampleBatch& batch, int32_t T) {
+    const size_t V = row.size(), rows = batch.size() * static_cast<size_t>(T);
+    if (rows * V > cap) {
+      if (dev) cudaFree(dev);
+      cap = rows * V;
+      cudaMalloc(&dev, sizeof(float) * cap);
+    }
+    std::vector<float> host(rows * V);
+    for (size_t r = 0; r < rows; ++r) std::memcpy(host.data() + r * V, row.data(), sizeof(float) * V);
+    cudaMemcpy(dev, host.data(), sizeof(float) * host.size(), cudaMemcpyHostToDevice);
+    return rlo_logits{dev, RLO_DTYPE_F32, static_cast<int32_t>(V), static_cast<int64_t>(V)};
+  }
+};
+
+}  // namespace
+
+int main() {
+  const int V = 37;
+  rng::Stream s(2506);
+  std::vector<float> row(V);
+  for (auto& z : row) z = static_cast<float>(1.5 * s.next_gaussian());
+  PolicyParams params;
+  params.layout = PolicyLayout{V, 1, 1, 1};
+  params.version = 1;
+  params.values.assign(params.layout.param_count(), 0.0);
+  for (int v = 0; v < V; ++v) params.values[params.layout.off_b2() + v] = row[static_cast<size_t>(v)];
+
+  // A batch in the reference's own currency (sample.hpp:16-33).
+  SampleBatch batch;
+  for (int i = 0; i < 7; ++i) {
+    SampleRecord r;
+    r.sample_id = "s" + std::to_string(i);
+    r.prompt_tokens = {1, 2};
+    const size_t n = 1 + s.next_below(9);
+    for (size_t t = 0; t < n; ++t) r.response_tokens.push_back(static_cast<int>(s.next_below(V)));
+    if (i % 2) {
+      for (size_t t = 0; t < n; ++t) r.action_mask.push_back(s.next_double() < 0.75 ? 1 : 0);
+      r.action_mask[0] = 1;
+    }
+    batch.push_back(r);
+  }
+  const auto lps = forward_logprobs(params, batch);
+  for (size_t i = 0; i < batch.size(); ++i) {
+    auto& r = batch.samples[i];
+    for (size_t t = 0; t < r.response_tokens.size(); ++t) {
+      r.response_logprobs.push_back(lps[i][t] + 0.4 * (2.0 * s.next_double() - 1.0));
+      r.ref_logprobs.push_back(lps[i][t] + 0.2 * (2.0 * s.next_double() - 1.0));
+      r.advantages.push_back(2.0 * s.next_double() - 1.0);
+      r.rewards.push_back(t + 1 == r.response_tokens.size() ? s.next_double() : 0.0);
+    }
+  }
+
+  TrainConfig cfg;
+  cfg.kl_coef = 0.1;
+  const Vocabulary& vocab = Vocabulary::standard();
+  (void)vocab;
+  TiledRow tiles{std::vector<float>(row)};
+  auto provider = [&tiles](const SampleBatch& b, int32_t T) { return tiles(b, T); };
+
+  PolicyWorker ref_worker(params, Vocabulary::standard(), cfg);
+  rollmini_b200::B200PolicyWorker b200(0, cfg, provider);
+
+  Message in;
+  in.batch = batch;
+  in.fields["version"] = "1";
+
+  // 1) forward_logprobs (policy_workers.cpp:93-100)
+  {
+    Message a = ref_worker.call("forward_logprobs", in);
+    Message b = b200.call("forward_logprobs", in);
+    double worst = 0.0;
+    for (size_t i = 0; i < batch.size(); ++i)
+      for (size_t t = 0; t < a.batch.samples[i].ref_logprobs.size(); ++t) {
+        const double g = b.batch.samples[i].ref_logprobs[t], r = a.batch.samples[i].ref_logprobs[t];
+        worst = std::max(worst, std::fabs(g - r) / std::max(1.0, std::fabs(r)));
+      }
+    check(worst <= 1e-5, "forward_logprobs reply matches the reference worker (max scaled err " +
+                             std::to_string(worst) + ")");
+  }
+
+  // 2) compute_gradient scalars (policy_workers.cpp:111-121) and the controller merge (policy.cpp:421-450)
+  {
+    Message a = ref_worker.call("compute_gradient", in);
+    Message b = b200.call("compute_gradient", in);
+    bool ok = true;
+    for (const char* k : {"loss_sum", "ratio_sum", "kl_sum"}) ok &= close(b.scalar(k), a.scalar(k));
+    ok &= b.scalar("clipped") == a.scalar("clipped") && b.scalar("tokens") == a.scalar("tokens");
+    check(ok, "compute_gradient scalars match (loss_sum " + std::to_string(b.scalar("loss_sum")) + " vs " +
+                  std::to_string(a.scalar("loss_sum")) + ", tokens " + std::to_string(b.scalar("tokens")) + ")");
+    GradAccum pa, pb;
+    pa.loss_sum = a.scalar("loss_sum");
+    pa.ratio_sum = a.scalar("ratio_sum");
+    pa.kl_sum = a.scalar("kl_sum");
+    pa.clipped = static_cast<size_t>(a.scalar("clipped"));
+    pa.tokens = static_cast<size_t>(a.scalar("tokens"));
+    pb.loss_sum = b.scalar("loss_sum");
+    pb.ratio_sum = b.scalar("ratio_sum");
+    pb.kl_sum = b.scalar("kl_sum");
+    pb.clipped = static_cast<size_t>(b.scalar("clipped"));
+    pb.tokens = static_cast<size_t>(b.scalar("tokens"));
+    const auto sa = merge_gradients({pa}).second, sb = merge_gradients({pb}).second;
+    check(close(sb.loss, sa.loss) && close(sb.mean_ratio, sa.mean_ratio) && close(sb.mean_kl, sa.mean_kl) &&
+              sb.tokens == sa.tokens,
+          "reference merge_gradients over B200 partials == over reference partials");
+    check(b.tensors.count("dlogp") == 1, "compute_gradient returns per-token dlogp");
+  }
+
+  // 3) compute_advantages (policy.cpp:257-311), whitening on
+  {
+    TrainConfig c2 = cfg;
+    c2.whiten_advantages = true;
+    c2.gamma = 0.95;
+    const auto ra = compute_advantages(batch, c2);
+    const auto ga = rollmini_b200::compute_advantages(b200.objective(), batch, c2);
+    double worst = 0.0;
+    for (size_t i = 0; i < ra.size(); ++i)
+      for (size_t t = 0; t < ra[i].size(); ++t)
+        worst = std::max(worst, std::fabs(ga[i][t] - ra[i][t]) / std::max(1.0, std::fabs(ra[i][t])));
+    check(worst <= 2e-5, "compute_advantages matches the reference (max scaled err " + std::to_string(worst) + ")");
+  }
+
+  // 4) error contracts: same exception classes and messages
+  {
+    Message bad = in;
+    bad.batch.samples[2].advantages.clear();
+    std::string ra, rb;
+    try {
+      ref_worker.call("compute_gradient", bad);
+    } catch (const InputError& e) {
+      ra = e.what();
+    }
+    try {
+      b200.call("compute_gradient", bad);
+    } catch (const InputError& e) {
+      rb = e.what();
+    }
+    check(!ra.empty() && ra == rb, "missing advantages -> InputError '" + rb + "'");
+    bool dispatch = false;
+    try {
+      b200.call("generate", in);
+    } catch (const DispatchError&) {
+      dispatch = true;
+    }
+    check(dispatch, "unknown method -> DispatchError");
+    Message oov = in;
+    oov.batch.samples[0].response_tokens[0] = V + 3;
+    std::string ea, eb;
+    try {
+      ref_worker.call("forward_logprobs", oov);
+    } catch (const InputError& e) {
+      ea = e.what();
+    }
+    try {
+      b200.call("forward_logprobs", oov);
+    } catch (const InputError& e) {
+      eb = e.what();
+    }
+    check(!ea.empty() && ea == eb, "OOV token -> InputError '" + eb + "'");
+  }
+
+  // 5) the reference's own Cluster driving B200 workers (thread per rank)
+  {
+    int ndev = 0;
+    cudaGetDeviceCount(&ndev);
+    std::vector<BindingAssignment> assign = {{0, "g0"}, {1, "g1"}};
+    auto factory = [&provider, &cfg, ndev](int rank, int world, const std::string&) -> std::unique_ptr<Worker> {
+      auto w = std::make_unique<rollmini_b200::B200PolicyWorker>(rank % std::max(ndev, 1), cfg, provider);
+      w->rank = rank;
+      w->world_size = world;
+      return w;
+    };
+    Cluster cluster(Role::reference, 2, assign, factory);
+    SampleBatch out = cluster_forward_logprobs(cluster, batch);
+    double worst = 0.0;
+    for (size_t i = 0; i < batch.size(); ++i)
+      for (size_t t = 0; t < lps[i].size(); ++t)
+        worst = std::max(worst, std::fabs(out.samples[i].ref_logprobs[t] - lps[i][t]) / std::max(1.0, std::fabs(lps[i][t])));
+    check(out.size() == batch.size() && worst <= 1e-5,
+          "reference Cluster + cluster_forward_logprobs over 2 B200 workers == reference forward_logprobs");
+  }
+
+  std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "OK", g_fail);
+  return g_fail ? 1 : 0;
+}
