@@ -420,6 +420,8 @@ def test_full_size_config2_properties(env):
     cfg1 = rlo.TrainConfig()
     obj.ppo_gradient(cfg1, toks, lengths, L[0], adv, old_logits=L[0])
     st1 = obj.merge_gradients(cfg1)
-    assert st1.mean_ratio == 1.0 and close(st1.loss, -float(adv.double().mean()), 1e-6)
+    # exactly 1 when both rows use the same exp2 path; within 1e-7 when RLO_VOCAB_MATH>=2 sends part of
+    # the old-policy row's exponentials through the FMA-pipe polynomial (relative error 1.9e-7 per term)
+    assert abs(st1.mean_ratio - 1.0) <= 1e-7 and close(st1.loss, -float(adv.double().mean()), 1e-6)
     del L
     torch.cuda.empty_cache()

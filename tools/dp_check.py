@@ -1,0 +1,99 @@
+"""Multi-GPU data-parallel parity check (run under torchrun, one process per GPU).
+
+Every rank takes its group-aligned shard (rlo_shard_plan) of one
+deterministic global batch, runs the whole path with an NCCL communicator
+(global whitening statistics and loss partials all-gathered, merged in rank
+order), and rank 0 compares against a single-GPU run of the full batch on its
+own device (a second handle without a communicator): advantages within 1e-6,
+stats within 1e-9 relative, counts exact — the reference's DP-equivalence
+property (test_policy.cpp:478-497).  Prints PASS/FAIL lines and
+exits non-zero on failure.
+
+    python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tools/dp_check.py
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2506_06122_b200 as rlo  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    B, T, V, G = 48, 64, 8192, 4
+    rng = np.random.default_rng(11)
+    lengths = rng.integers(T // 4, T + 1, B).astype(np.int32)
+    mask = (rng.random((B, T)) < 0.9).astype(np.uint8)
+    rs = rng.integers(0, 2, B).astype(np.float32)
+    cfgs = {
+        "grpo+whiten+group-mean": rlo.TrainConfig(adv_estimator="grpo", group_size=G, whiten_advantages=True,
+                                                  kl_coef=0.01, kl_estimator="k3", loss_agg="group-mean",
+                                                  dual_clip_c=3.0),
+        "gae+whiten+seq-mean": rlo.TrainConfig(adv_estimator="gae", group_size=G, whiten_advantages=True,
+                                               gamma=0.99, lambd=0.95, kl_coef=0.05, kl_estimator="k2",
+                                               loss_agg="seq-mean-token-mean"),
+    }
+    rt = (rng.standard_normal((B, T)) * 0.2).astype(np.float32)
+    vals = (rng.standard_normal((B, T)) * 0.5).astype(np.float32)
+    full = [torch.empty(B * T, V, dtype=torch.bfloat16, device=dev) for _ in range(3)]
+    for m in range(3):
+        rlo.synth_logits(full[m], seed=3, model=m)
+    toks = torch.empty(B, T, dtype=torch.int32, device=dev)
+    rlo.synth_tokens(toks, V, seed=3)
+
+    obj = rlo.Objective(local)
+    uid = [rlo.Objective.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    obj.init_comm(uid[0], rank, world)
+    b0, n = rlo.shard_plan(B, G, world, rank)
+    fails = 0
+    for name, cfg in cfgs.items():
+        d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        kw = dict(rewards=d(rt[b0:b0 + n]), values=d(vals[b0:b0 + n])) if cfg.adv_estimator == "gae" else \
+            dict(scalar_rewards=d(rs[b0:b0 + n]))
+        adv = obj.compute_advantages(cfg, d(lengths[b0:b0 + n]), T=T, mask=d(mask[b0:b0 + n]), **kw)
+        rows = slice(b0 * T, (b0 + n) * T)
+        obj.ppo_gradient(cfg, toks[b0:b0 + n].contiguous(), d(lengths[b0:b0 + n]), full[0][rows], adv,
+                         mask=d(mask[b0:b0 + n]), old_logits=full[1][rows], ref_logits=full[2][rows])
+        st = obj.merge_gradients(cfg)
+        gathered = [torch.zeros(B, T, device=dev) for _ in range(world)] if rank == 0 else None
+        pad = torch.zeros(B, T, device=dev)
+        pad[:n] = adv
+        dist.gather(pad, gathered, dst=0)
+        counts = [None] * world
+        dist.all_gather_object(counts, n)
+        if rank == 0:
+            single = rlo.Objective(local)
+            kw1 = dict(rewards=d(rt), values=d(vals)) if cfg.adv_estimator == "gae" else dict(scalar_rewards=d(rs))
+            adv1 = single.compute_advantages(cfg, d(lengths), T=T, mask=d(mask), **kw1)
+            single.ppo_gradient(cfg, toks, d(lengths), full[0], adv1, mask=d(mask), old_logits=full[1],
+                                ref_logits=full[2])
+            st1 = single.merge_gradients(cfg)
+            adv_dp = torch.cat([g[:c] for g, c in zip(gathered, counts)])
+            a_err = float((adv_dp - adv1).abs().max())
+            ok = a_err <= 1e-6
+            for k in ("loss", "mean_ratio", "clip_fraction", "mean_kl", "mean_entropy", "dual_clip_fraction"):
+                g, r = getattr(st, k), getattr(st1, k)
+                ok &= abs(g - r) <= 1e-9 * max(1.0, abs(r))
+            ok &= (st.tokens, st.seqs, st.groups) == (st1.tokens, st1.seqs, st1.groups)
+            print(f"{'PASS' if ok else 'FAIL'} dp{world} {name}: loss {st.loss:.12f} vs single {st1.loss:.12f}, "
+                  f"adv max err {a_err:.2e}, tokens {st.tokens}", flush=True)
+            fails += not ok
+            single.close()
+    obj.close()
+    flag = torch.tensor([fails], device=dev)
+    dist.broadcast(flag, src=0)
+    dist.destroy_process_group()
+    sys.exit(1 if int(flag.item()) else 0)
+
+
+if __name__ == "__main__":
+    main()
