@@ -122,7 +122,16 @@ typedef struct rlo_token_out {
   float* entropy;   /* actor entropy of the position */
   float* dlogp;     /* d(loss_t)/d(logp_t), policy.cpp:372-374 */
   float* loss;      /* per-token loss contribution (0 for non-participating tokens) */
+  float* lse;       /* actor log-sum-exp of the row (input of rlo_logits_backward) */
 } rlo_token_out;
+
+/* Critic value-loss statistics (value_gradient, policy.cpp:474-540). */
+typedef struct rlo_value_stats {
+  double loss;           /* token-mean of 0.5*err^2 (clipped form when value_clip > 0) */
+  double clip_fraction;  /* tokens where the clipped branch was taken */
+  double mean_value;
+  uint64_t tokens;
+} rlo_value_stats;
 
 /* UpdateStats (include/rollmini/policy.hpp:130-136) plus extension stats. */
 typedef struct rlo_stats {
@@ -278,6 +287,37 @@ rlo_status rlo_objective_step_host(rlo_handle* h, const rlo_train_config* cfg, i
                                    const float* old_logp, const float* ref_logp,
                                    float* host_adv_out, float* host_logp_out, rlo_stats* stats,
                                    void* stream);
+
+/* ---- next rows: the callers either side of the path ------ */
+
+/* Aggregation weight of every loss-participating token (0 elsewhere): the
+ * factor from d(loss_t)/d(logp_t) to d(L)/d(logp_t) under cfg.loss_agg, using
+ * the merged (global) counts of `stats` (from rlo_merge_gradients):
+ * token-mean 1/tokens (policy.cpp:438-440), seq-mean-token-mean
+ * 1/(seqs*m_b), seq-mean-token-sum 1/seqs, group-mean 1/(groups*M_g), with
+ * m_b / M_g the participating tokens of the sample / group.  out_w [B*T]. */
+rlo_status rlo_loss_weights(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch,
+                            const rlo_stats* stats, float* out_w, void* stream);
+
+/* Actor backward epilogue (policy.cpp:375-379): for every row with
+ * weight*dlogp != 0, grad[v] = weight*dlogp*(1[v == token] - exp(z_v - lse)),
+ * recomputing the softmax from the row and its lse (never stored); all
+ * other rows of `grad` are zeroed.  grad has grad_dtype (rlo_dtype) and
+ * grad_row_stride; lse / dlogp / weight are [B*T] (rlo_token_out.lse,
+ * rlo_token_out.dlogp, rlo_loss_weights). */
+rlo_status rlo_logits_backward(rlo_handle* h, const rlo_batch* batch, const rlo_logits* logits, const float* lse,
+                               const float* dlogp, const float* weight, void* grad, int32_t grad_dtype,
+                               int64_t grad_row_stride, void* stream);
+
+/* Critic value loss (value_gradient, policy.cpp:474-540): per
+ * loss-participating token err = v - return, loss 0.5*err^2, d/dv = err.
+ * With old_values and value_clip > 0: the clipped PPO value loss
+ * 0.5*max((v-R)^2, (v_old + clamp(v - v_old, +-c) - R)^2).  Reduced over the
+ * communicator like merge_gradients.  out_dvalue [B*T] optional (0 off-mask).
+ * Synchronises `stream`; TrainingError when no token participates. */
+rlo_status rlo_value_loss(rlo_handle* h, const rlo_batch* batch, const float* values, const float* old_values,
+                          const float* returns, double value_clip, float* out_dvalue, rlo_value_stats* out,
+                          void* stream);
 
 /* Synchronise `stream` and report device-side input errors (OOV tokens). */
 rlo_status rlo_sync(rlo_handle* h, void* stream);

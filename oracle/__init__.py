@@ -289,3 +289,50 @@ def ref_split_sizes(n, parts):
     out = np.zeros(parts, dtype=np.int64)
     ref().ref_split_sizes(C.c_int64(n), C.c_int32(parts), _p(out))
     return out
+
+
+# ---- aggregation weights, actor backward, value loss ---------------------------
+
+def loss_weights(cfg, B, T, lengths, mask=None):
+    lengths, mask = _i32(lengths), _u8(mask)
+    out = np.zeros(B * T)
+    lib().orc_loss_weights(C.byref(cfg), C.c_int32(B), C.c_int32(T), _p(lengths), _p(mask), _p(out))
+    return out
+
+
+def logits_backward_row(z, tok, scale):
+    z = _f64(z)
+    out = np.zeros(z.size)
+    lib().orc_logits_backward_row(_p(z), C.c_int32(z.size), C.c_int32(tok), C.c_double(scale), _p(out))
+    return out
+
+
+def value_loss(B, T, lengths, mask, values, old_values, returns, value_clip=0.0):
+    lengths, mask = _i32(lengths), _u8(mask)
+    values, old_values, returns = _f64(values), _f64(old_values), _f64(returns)
+    dv, out4 = np.zeros(B * T), np.zeros(4)
+    lib().orc_value_loss(C.c_int32(B), C.c_int32(T), _p(lengths), _p(mask), _p(values), _p(old_values),
+                         _p(returns), C.c_double(value_clip), _p(dv), _p(out4))
+    return dv, dict(zip(["loss_sum", "tokens", "clipped", "value_sum"], out4.tolist()))
+
+
+def ref_ppo_grad_b2(row, B, T, lengths, tokens, mask, old_lp, ref_lp, adv, cfg, world=1):
+    row, lengths, tokens, mask = _f64(row), _i32(lengths), _i32(tokens), _u8(mask)
+    old_lp, ref_lp, adv = _f64(old_lp), _f64(ref_lp), _f64(adv)
+    out = np.zeros(row.size)
+    err = C.create_string_buffer(512)
+    code = ref().ref_ppo_grad_b2(_p(row), C.c_int32(row.size), C.c_int32(B), C.c_int32(T), _p(lengths),
+                                 _p(tokens), _p(mask), _p(old_lp), _p(ref_lp), _p(adv), C.byref(cfg),
+                                 C.c_int32(world), _p(out), err, C.c_int32(512))
+    _check(code, err)
+    return out
+
+
+def ref_value_loss_b2(vb, B, T, lengths, mask, targets):
+    lengths, mask, targets = _i32(lengths), _u8(mask), _f64(targets)
+    out = np.zeros(3)
+    err = C.create_string_buffer(512)
+    code = ref().ref_value_loss_b2(C.c_double(vb), C.c_int32(B), C.c_int32(T), _p(lengths), _p(mask),
+                                   _p(targets), _p(out), err, C.c_int32(512))
+    _check(code, err)
+    return dict(zip(["loss_sum", "tokens", "grad_vb"], out.tolist()))

@@ -360,6 +360,78 @@ void orc_split_sizes(int64_t n, int32_t parts, int64_t* out) { /* sample.cpp:99-
   for (int64_t i = 0; i < n % parts; ++i) ++out[i];
 }
 
+/* ---- aggregation weights, actor backward, value loss ------------------------ */
+void orc_loss_weights(const rlo_train_config* cfg, int32_t B, int32_t T, const int32_t* lengths,
+                      const uint8_t* mask, double* out_w) {
+  const int32_t G = cfg->group_size > 0 ? cfg->group_size : 1;
+  double tokens = 0.0, seqs = 0.0, groups = 0.0;
+  double* m = (double*)calloc((size_t)(B > 0 ? B : 1), sizeof(double));
+  for (int32_t b = 0; b < B; ++b) {
+    for (int32_t t = 0; t < lengths[b]; ++t) m[b] += mask_at(mask, (int64_t)b * T + t) ? 1.0 : 0.0;
+    tokens += m[b];
+    seqs += m[b] > 0.0;
+  }
+  double* M = (double*)calloc((size_t)(B / G + 2), sizeof(double));
+  for (int32_t b = 0; b < B; ++b) M[b / G] += m[b];
+  for (int32_t g = 0; g * G < B; ++g) groups += M[g] > 0.0;
+  for (int32_t b = 0; b < B; ++b)
+    for (int32_t t = 0; t < T; ++t) {
+      const int64_t i = (int64_t)b * T + t;
+      double w = 0.0;
+      if (t < lengths[b] && mask_at(mask, i)) {
+        switch (cfg->loss_agg) {
+          case RLO_AGG_SEQ_MEAN_TOKEN_MEAN: w = 1.0 / (seqs * m[b]); break;
+          case RLO_AGG_SEQ_MEAN_TOKEN_SUM: w = 1.0 / seqs; break;
+          case RLO_AGG_GROUP_MEAN: w = 1.0 / (groups * M[b / G]); break;
+          default: w = 1.0 / tokens; break;
+        }
+      }
+      out_w[i] = w;
+    }
+  free(m);
+  free(M);
+}
+
+void orc_logits_backward_row(const double* z, int32_t V, int32_t tok, double scale, double* out) {
+  double lse;
+  orc_logsoftmax_row(z, V, &lse, NULL);
+  for (int32_t v = 0; v < V; ++v) out[v] = scale * ((v == tok ? 1.0 : 0.0) - exp(z[v] - lse));
+}
+
+void orc_value_loss(int32_t B, int32_t T, const int32_t* lengths, const uint8_t* mask, const double* values,
+                    const double* old_values, const double* returns, double value_clip, double* out_dv,
+                    double* out4) {
+  double loss = 0.0, tokens = 0.0, clipped = 0.0, vsum = 0.0;
+  for (int64_t i = 0; i < (int64_t)B * T; ++i) out_dv[i] = 0.0;
+  for (int32_t b = 0; b < B; ++b)
+    for (int32_t t = 0; t < lengths[b]; ++t) {
+      const int64_t i = (int64_t)b * T + t;
+      if (!mask_at(mask, i)) continue; /* policy.cpp:501-504 */
+      const double v = values[i], R = returns[i];
+      const double err = v - R; /* :508 */
+      double l = 0.5 * err * err, d = err;
+      if (old_values && value_clip > 0.0) {
+        const double dv = v - old_values[i];
+        const double vc = old_values[i] + clampd(dv, -value_clip, value_clip);
+        const double errc = vc - R;
+        const double lc = 0.5 * errc * errc;
+        if (lc > l) {
+          l = lc;
+          d = (dv > -value_clip && dv < value_clip) ? errc : 0.0;
+          clipped += 1.0;
+        }
+      }
+      loss += l; /* :509 */
+      tokens += 1.0; /* :510 */
+      vsum += v;
+      out_dv[i] = d; /* :512 */
+    }
+  out4[0] = loss;
+  out4[1] = tokens;
+  out4[2] = clipped;
+  out4[3] = vsum;
+}
+
 /* ---- synthetic inputs (include/rlo_synth.h) -------------------------------- */
 static void synth_row_f(float* out, int32_t V, uint64_t seed, int32_t model, uint64_t row_key) {
   int32_t spikes[RLO_SYNTH_SPIKES];

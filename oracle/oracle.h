@@ -63,6 +63,26 @@ int32_t orc_merge(const rlo_partials* parts, int32_t nranks, const rlo_train_con
 /* sample.cpp:99-105 */
 void orc_split_sizes(int64_t n, int32_t parts, int64_t* out);
 
+/* Aggregation weight of every loss-participating token (0 elsewhere): the
+ * factor turning d(loss_t)/d(logp_t) into d(L)/d(logp_t) for cfg->loss_agg
+ * (token-mean: 1/tokens, policy.cpp:438-440; seq-mean-token-mean:
+ * 1/(seqs*m_b); seq-mean-token-sum: 1/seqs; group-mean: 1/(groups*M_g)). */
+void orc_loss_weights(const rlo_train_config* cfg, int32_t B, int32_t T, const int32_t* lengths,
+                      const uint8_t* mask, double* out_w);
+
+/* Actor backward epilogue restated from policy.cpp:376-379:
+ * dz[v] = scale * (1[v == tok] - exp(z_v - lse)), scale = w_t * dlogp_t. */
+void orc_logits_backward_row(const double* z, int32_t V, int32_t tok, double scale, double* out);
+
+/* Critic value loss, value_gradient restated (policy.cpp:500-512): per
+ * loss-participating token err = v - target, loss 0.5*err^2, d/dv = err.
+ * Extension: with old_values and value_clip > 0, the clipped PPO value loss
+ * 0.5*max((v-R)^2, (v_old + clamp(v - v_old, +-c) - R)^2).
+ * out4 = {loss_sum, tokens, clipped, sum of values}; out_dv per token (0 off-mask). */
+void orc_value_loss(int32_t B, int32_t T, const int32_t* lengths, const uint8_t* mask, const double* values,
+                    const double* old_values, const double* returns, double value_clip, double* out_dv,
+                    double* out4);
+
 /* Synthetic row / token of include/rlo_synth.h, as doubles (bf16-rounded
  * when dtype is bf16). */
 void orc_synth_row(double* out, int32_t dtype, int32_t V, uint64_t seed, int32_t model, uint64_t row_key);

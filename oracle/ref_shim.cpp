@@ -172,6 +172,42 @@ int32_t ref_ppo_stats_b2(const double* row, int32_t V, int32_t B, int32_t T, con
   });
 }
 
+// The same ppo_gradient -> merge_gradients run, returning the merged
+// gradient's b2 segment: with every position's logits = b2, d(loss)/d(b2) is
+// the token-mean sum over tokens of dz = dlp * (onehot - softmax)
+// (policy.cpp:375-379, :391, :439-440) — the actor backward epilogue.
+int32_t ref_ppo_grad_b2(const double* row, int32_t V, int32_t B, int32_t T, const int32_t* lengths,
+                        const int32_t* tokens, const uint8_t* mask, const double* old_lp, const double* ref_lp,
+                        const double* adv, const rlo_train_config* cfg, int32_t world, double* out_grad_b2,
+                        char* err, int32_t errlen) {
+  return guarded(err, errlen, [&] {
+    PolicyParams p = b2_params(V);
+    std::memcpy(p.values.data() + p.layout.off_b2(), row, sizeof(double) * V);
+    SampleBatch batch = make_batch(B, T, lengths, tokens, mask, nullptr, nullptr, old_lp, ref_lp, adv);
+    auto shards = split_batch(batch, static_cast<size_t>(world));
+    std::vector<GradAccum> parts;
+    for (const auto& s : shards) parts.push_back(ppo_gradient(p, s, to_ref(cfg)));
+    auto [grad, stats] = merge_gradients(parts);
+    std::memcpy(out_grad_b2, grad.data() + p.layout.off_b2(), sizeof(double) * V);
+  });
+}
+
+// value_gradient (policy.cpp:474-540) with every position's value = vb
+// (all parameters 0 except the value-head bias vb): out3 = {loss_sum, tokens,
+// d(loss_sum)/d(vb) = sum of err}.
+int32_t ref_value_loss_b2(double vb, int32_t B, int32_t T, const int32_t* lengths, const uint8_t* mask,
+                          const double* targets, double* out3, char* err, int32_t errlen) {
+  return guarded(err, errlen, [&] {
+    PolicyParams p = b2_params(4);
+    p.values[p.layout.off_vb()] = vb;
+    SampleBatch batch = make_batch(B, T, lengths, nullptr, mask, nullptr, nullptr, nullptr, nullptr, targets);
+    GradAccum acc = value_gradient(p, batch);
+    out3[0] = acc.loss_sum;
+    out3[1] = static_cast<double>(acc.tokens);
+    out3[2] = acc.grad[p.layout.off_vb()];
+  });
+}
+
 // merge_gradients (policy.cpp:421-450) on scalar partials with empty grads.
 int32_t ref_merge_scalars(const double* parts5, int32_t nranks, double* out5, char* err, int32_t errlen) {
   return guarded(err, errlen, [&] {

@@ -43,7 +43,7 @@ class rlo_logits(C.Structure):
 
 class rlo_token_out(C.Structure):
     _fields_ = [("logp", C.c_void_p), ("old_logp", C.c_void_p), ("ref_logp", C.c_void_p),
-                ("entropy", C.c_void_p), ("dlogp", C.c_void_p), ("loss", C.c_void_p)]
+                ("entropy", C.c_void_p), ("dlogp", C.c_void_p), ("loss", C.c_void_p), ("lse", C.c_void_p)]
 
 
 class rlo_stats(C.Structure):
@@ -52,6 +52,11 @@ class rlo_stats(C.Structure):
         ("mean_kl", C.c_double), ("tokens", C.c_uint64), ("mean_entropy", C.c_double),
         ("dual_clip_fraction", C.c_double), ("seqs", C.c_uint64), ("groups", C.c_uint64),
     ]
+
+
+class rlo_value_stats(C.Structure):
+    _fields_ = [("loss", C.c_double), ("clip_fraction", C.c_double), ("mean_value", C.c_double),
+                ("tokens", C.c_uint64)]
 
 
 class rlo_partials(C.Structure):
@@ -106,6 +111,9 @@ def lib() -> C.CDLL:
         "rlo_objective_step_host": ([vp, P(rlo_train_config), i32, i32, vp, vp, vp, vp, vp, vp, P(rlo_logits),
                                      P(rlo_logits), P(rlo_logits), vp, vp, vp, vp, P(rlo_stats), vp], C.c_int),
         "rlo_sync": ([vp, vp], C.c_int),
+        "rlo_loss_weights": ([vp, P(rlo_train_config), P(rlo_batch), P(rlo_stats), vp, vp], C.c_int),
+        "rlo_logits_backward": ([vp, P(rlo_batch), P(rlo_logits), vp, vp, vp, vp, i32, i64, vp], C.c_int),
+        "rlo_value_loss": ([vp, P(rlo_batch), vp, vp, vp, C.c_double, vp, P(rlo_value_stats), vp], C.c_int),
         "rlo_synth_logits": ([vp, i32, i64, i32, i64, u64, i32, i64, vp], C.c_int),
         "rlo_synth_tokens": ([vp, i64, i32, u64, i64, i64, vp], C.c_int),
     }

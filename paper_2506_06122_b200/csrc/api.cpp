@@ -152,6 +152,9 @@ struct rlo_handle {
   // whitening
   DevBuf<WStat> wstat;
   DevBuf<double> raw64;
+  // next-row callers: loss weights, value loss
+  DevBuf<float> counts;
+  DevBuf<double> vseq, vout, vgath;
   DevBuf<double> stats4, stats_all, partials, gathered;
   DevBuf<DevError> err;
   // staging for rlo_objective_step_host and internal advantages
@@ -328,6 +331,10 @@ rlo_status rlo_destroy(rlo_handle* h) {
   h->s_flags.release();
   h->wstat.release();
   h->raw64.release();
+  h->counts.release();
+  h->vseq.release();
+  h->vout.release();
+  h->vgath.release();
   h->stats4.release();
   h->stats_all.release();
   h->partials.release();
@@ -590,6 +597,7 @@ rlo_status rlo_ppo_gradient(rlo_handle* h, const rlo_train_config* cfg, const rl
     a.o_ent = out->entropy;
     a.o_dlogp = out->dlogp;
     a.o_loss = out->loss;
+    a.o_lse = out->lse;
   }
   a.s_loss = h->s_loss.p;
   a.s_ratio = h->s_ratio.p;
@@ -720,6 +728,74 @@ rlo_status rlo_objective_step_host(rlo_handle* h, const rlo_train_config* cfg, i
   if (host_logp_out && N)
     RLO_CUDA(cudaMemcpyAsync(host_logp_out, h->h_logp.p, sizeof(float) * N, cudaMemcpyDeviceToHost, s));
   return rlo_merge_gradients(h, cfg, stats, nullptr, stream);  // synchronises the stream
+}
+
+rlo_status rlo_loss_weights(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch, const rlo_stats* stats,
+                            float* out_w, void* stream) {
+  if (!h) return fail(RLO_ERR_INPUT, "loss_weights: null handle");
+  RLO_TRY(rlo_train_config_validate(cfg));
+  RLO_TRY(check_batch(batch, "loss_weights", false));
+  if (!stats || !out_w) return fail(RLO_ERR_INPUT, "loss_weights: stats and out_w required");
+  if (stats->tokens == 0) return fail(RLO_ERR_TRAINING, "merge_gradients: batch contains no loss-participating tokens");
+  DeviceGuard g(h->device);
+  RLO_CUDA(h->counts.ensure(static_cast<size_t>(batch->B > 0 ? batch->B : 1)));
+  RLO_CUDA(launch_loss_weights(batch->B, batch->T, cfg->group_size, cfg->loss_agg, (double)stats->tokens,
+                               (double)stats->seqs, (double)stats->groups, batch->lengths, batch->mask, h->counts.p,
+                               out_w, static_cast<cudaStream_t>(stream)));
+  return RLO_OK;
+}
+
+rlo_status rlo_logits_backward(rlo_handle* h, const rlo_batch* batch, const rlo_logits* logits, const float* lse,
+                               const float* dlogp, const float* weight, void* grad, int32_t grad_dtype,
+                               int64_t grad_row_stride, void* stream) {
+  if (!h) return fail(RLO_ERR_INPUT, "logits_backward: null handle");
+  RLO_TRY(check_batch(batch, "logits_backward", true));
+  RLO_TRY(check_logits(logits, "logits_backward", "actor"));
+  if ((int64_t)batch->B * batch->T == 0) return RLO_OK;
+  if (!lse || !dlogp || !weight || !grad) return fail(RLO_ERR_INPUT, "logits_backward: lse, dlogp, weight, grad required");
+  if (grad_dtype != RLO_DTYPE_F32 && grad_dtype != RLO_DTYPE_BF16)
+    return fail(RLO_ERR_INPUT, "logits_backward: unsupported grad dtype");
+  if (grad_row_stride < logits->V) return fail(RLO_ERR_INPUT, "logits_backward: grad row stride < V");
+  DeviceGuard g(h->device);
+  RLO_CUDA(launch_logits_backward(logits->data, logits->dtype, logits->row_stride, logits->V, batch->B, batch->T,
+                                  batch->lengths, batch->tokens, lse, dlogp, weight, grad, grad_dtype, grad_row_stride,
+                                  h->num_sms, static_cast<cudaStream_t>(stream)));
+  return RLO_OK;
+}
+
+rlo_status rlo_value_loss(rlo_handle* h, const rlo_batch* batch, const float* values, const float* old_values,
+                          const float* returns, double value_clip, float* out_dvalue, rlo_value_stats* out,
+                          void* stream) {
+  if (!h) return fail(RLO_ERR_INPUT, "value_loss: null handle");
+  RLO_TRY(check_batch(batch, "value_loss", false));
+  const int32_t B = batch->B, T = batch->T;
+  if ((int64_t)B * T > 0 && (!values || !returns))  // policy.cpp:497-498
+    return fail(RLO_ERR_INPUT, "value_gradient: sample '0' missing targets");
+  if (!(value_clip >= 0.0)) return fail(RLO_ERR_CONFIG, "value_loss: value_clip must be non-negative");
+  DeviceGuard g(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  RLO_CUDA(h->vseq.ensure(static_cast<size_t>(4 * (B > 0 ? B : 1))));
+  RLO_CUDA(h->vout.ensure(4));
+  RLO_CUDA(launch_value_loss(B, T, batch->lengths, batch->mask, values, old_values, returns, value_clip, out_dvalue,
+                             h->vseq.p, h->vout.p, s));
+  const int world = h->comm ? h->world : 1;
+  if (h->comm) {
+    RLO_CUDA(h->vgath.ensure(static_cast<size_t>(4 * world)));
+    RLO_NCCL(nccl_api().AllGather(h->vout.p, h->vgath.p, 4, ncclFloat64, h->comm, s));
+    RLO_CUDA(cudaMemcpyAsync(h->host_gathered, h->vgath.p, sizeof(double) * 4 * world, cudaMemcpyDeviceToHost, s));
+  } else {
+    RLO_CUDA(cudaMemcpyAsync(h->host_gathered, h->vout.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, s));
+  }
+  RLO_CUDA(cudaStreamSynchronize(s));
+  double sum[4] = {0, 0, 0, 0};
+  for (int r = 0; r < world; ++r)  // rank order
+    for (int k = 0; k < 4; ++k) sum[k] += h->host_gathered[4 * r + k];
+  if (sum[1] == 0.0) return fail(RLO_ERR_TRAINING, "value_loss: batch contains no loss-participating tokens");
+  const double inv = 1.0 / sum[1];
+  rlo_value_stats st{sum[0] * inv, sum[2] * inv, sum[3] * inv, static_cast<uint64_t>(sum[1])};
+  if (!std::isfinite(st.loss)) return fail(RLO_ERR_TRAINING, "value_loss: non-finite loss");
+  if (out) *out = st;
+  return RLO_OK;
 }
 
 rlo_status rlo_synth_logits(void* dst, int32_t dtype, int64_t rows, int32_t V, int64_t row_stride, uint64_t seed,

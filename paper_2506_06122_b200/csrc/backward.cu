@@ -1,0 +1,206 @@
+// backward.cu — the callers after the loss: the
+// aggregation weights d(L)/d(loss_t) and the actor backward epilogue
+// dlogits = w*dlogp*(onehot - softmax) (policy.cpp:375-379).
+//
+// logits_backward_kernel streams each row once (128-bit loads, the same
+// persistent 256-thread layout as the LDG vocab pass), recomputes
+// p_v = 2^(z_v*log2e - lse*log2e) from the forward pass's lse, and writes the
+// gradient row with streaming 128-bit stores (fp32 or bf16).  HBM-bound:
+// V*(s_in + s_out) bytes per row.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace rlo {
+namespace {
+
+constexpr int kBwThreads = 256;
+
+__global__ void seq_count_kernel(int B, int T, const int32_t* __restrict__ lengths, const uint8_t* __restrict__ mask,
+                                 float* __restrict__ counts) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (b >= B) return;
+  const int n = seq_len(lengths, b, T);
+  int c = 0;
+  for (int t = lane; t < n; t += 32) c += (!mask || mask[(int64_t)b * T + t]) ? 1 : 0;
+  c = warp_sum(c);
+  if (lane == 0) counts[b] = (float)c;
+}
+
+__global__ void loss_weight_kernel(int B, int T, int G, int agg, double tokens, double seqs, double groups,
+                                   const int32_t* __restrict__ lengths, const uint8_t* __restrict__ mask,
+                                   const float* __restrict__ counts, float* __restrict__ w) {
+  const int64_t N = (int64_t)B * T;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(i / T), t = (int)(i - (int64_t)b * T);
+    double x = 0.0;
+    if (t < seq_len(lengths, b, T) && (!mask || mask[i])) {
+      if (agg == RLO_AGG_SEQ_MEAN_TOKEN_MEAN) {
+        x = 1.0 / (seqs * (double)counts[b]);
+      } else if (agg == RLO_AGG_SEQ_MEAN_TOKEN_SUM) {
+        x = 1.0 / seqs;
+      } else if (agg == RLO_AGG_GROUP_MEAN) {
+        const int g0 = (b / G) * G, g1 = min(B, g0 + G);
+        double M = 0.0;
+        for (int k = g0; k < g1; ++k) M += (double)counts[k];
+        x = 1.0 / (groups * M);
+      } else {
+        x = 1.0 / tokens;
+      }
+    }
+    w[i] = (float)x;
+  }
+}
+
+struct BwArgs {
+  const void* logits;
+  int64_t stride;
+  int32_t V, B, T;
+  const int32_t* lengths;
+  const int32_t* tokens;
+  const float* lse;
+  const float* dlogp;
+  const float* weight;
+  void* grad;
+  int64_t gstride;
+};
+
+template <typename ET>
+struct In;
+template <>
+struct In<float> {
+  static constexpr int kN = 4;
+  __device__ static void load(const float* p, float (&z)[8]) {
+    const float4 v = ld_stream(reinterpret_cast<const float4*>(p));
+    z[0] = v.x, z[1] = v.y, z[2] = v.z, z[3] = v.w;
+  }
+  __device__ static float one(const float* p) { return __ldg(p); }
+};
+template <>
+struct In<__nv_bfloat16> {
+  static constexpr int kN = 8;
+  __device__ static void load(const __nv_bfloat16* p, float (&z)[8]) {
+    const uint4 v = ld_stream(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) z[2 * k] = bf16lo(w[k]), z[2 * k + 1] = bf16hi(w[k]);
+  }
+  __device__ static float one(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+};
+
+template <typename GT>
+struct Out;
+template <>
+struct Out<float> {
+  template <int N>
+  __device__ static void store(float* p, const float (&g)[8]) {
+    __stcs(reinterpret_cast<float4*>(p), make_float4(g[0], g[1], g[2], g[3]));
+    if (N == 8) __stcs(reinterpret_cast<float4*>(p) + 1, make_float4(g[4], g[5], g[6], g[7]));
+  }
+  __device__ static void one(float* p, float g) { p[0] = g; }
+};
+template <>
+struct Out<__nv_bfloat16> {
+  __device__ static uint32_t pack(float lo, float hi) {
+    return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(lo)) |
+           ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(hi)) << 16);
+  }
+  template <int N>
+  __device__ static void store(__nv_bfloat16* p, const float (&g)[8]) {
+    if (N == 8)
+      __stcs(reinterpret_cast<uint4*>(p), make_uint4(pack(g[0], g[1]), pack(g[2], g[3]), pack(g[4], g[5]), pack(g[6], g[7])));
+    else
+      __stcs(reinterpret_cast<uint2*>(p), make_uint2(pack(g[0], g[1]), pack(g[2], g[3])));
+  }
+  __device__ static void one(__nv_bfloat16* p, float g) { p[0] = __float2bfloat16_rn(g); }
+};
+
+template <typename ET, typename GT>
+__global__ void __launch_bounds__(kBwThreads) logits_backward_kernel(const BwArgs a, bool vec_ok) {
+  constexpr int N = In<ET>::kN;
+  const int64_t nrows = (int64_t)a.B * a.T;
+  const int nvec = vec_ok ? a.V / N : 0;
+  for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
+    const int b = (int)(row / a.T), t = (int)(row - (int64_t)b * a.T);
+    const bool valid = t < seq_len(a.lengths, b, a.T);
+    const float scale = valid ? __ldg(a.weight + row) * __ldg(a.dlogp + row) : 0.f;
+    GT* g = reinterpret_cast<GT*>(a.grad) + row * a.gstride;
+    const ET* z = reinterpret_cast<const ET*>(a.logits) + row * a.stride;
+    if (scale == 0.f) {  // non-participating (or zero-gradient) row: zeros
+      float zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int i = threadIdx.x; i < nvec; i += kBwThreads) Out<GT>::template store<N>(g + (int64_t)i * N, zero);
+      for (int v = nvec * N + threadIdx.x; v < a.V; v += kBwThreads) Out<GT>::one(g + v, 0.f);
+      continue;
+    }
+    const int tok = __ldg(a.tokens + row);
+    const float nl = -__ldg(a.lse + row) * kL2E;
+    const float ms = -scale;
+    for (int i = threadIdx.x; i < nvec; i += kBwThreads) {
+      float x[8], o[8];
+      In<ET>::load(z + (int64_t)i * N, x);
+#pragma unroll
+      for (int k = 0; k < N; ++k) o[k] = ms * ex2(fmaf(x[k], kL2E, nl));  // -w*dlp*p_v
+      const int d = tok - i * N;
+      if (d >= 0 && d < N) {
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+          if (k == d) o[k] += scale;  // + w*dlp at the realised token
+      }
+      Out<GT>::template store<N>(g + (int64_t)i * N, o);
+    }
+    for (int v = nvec * N + threadIdx.x; v < a.V; v += kBwThreads) {
+      float o = ms * ex2(fmaf(In<ET>::one(z + v), kL2E, nl));
+      if (v == tok) o += scale;
+      Out<GT>::one(g + v, o);
+    }
+  }
+}
+
+template <typename ET, typename GT>
+cudaError_t launch_bw(const BwArgs& a, int num_sms, cudaStream_t s) {
+  const int64_t nrows = (int64_t)a.B * a.T;
+  if (nrows == 0) return cudaSuccess;
+  constexpr int N = In<ET>::kN;
+  constexpr int64_t kOutAlign = N * sizeof(GT) < 16 ? N * sizeof(GT) : 16;  // widest store used
+  const bool vec_ok = (reinterpret_cast<uintptr_t>(a.logits) % 16 == 0) &&
+                      (reinterpret_cast<uintptr_t>(a.grad) % kOutAlign == 0) &&
+                      ((a.stride * (int64_t)sizeof(ET)) % 16 == 0) && ((a.gstride * (int64_t)sizeof(GT)) % kOutAlign == 0);
+  auto kern = logits_backward_kernel<ET, GT>;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBwThreads, 0);
+  int64_t grid = (int64_t)num_sms * (per_sm < 1 ? 1 : per_sm);
+  if (grid > nrows) grid = nrows;
+  kern<<<(int)grid, kBwThreads, 0, s>>>(a, vec_ok);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_loss_weights(int32_t B, int32_t T, int32_t G, int32_t agg, double tokens, double seqs,
+                                double groups, const int32_t* lengths, const uint8_t* mask, float* counts, float* w,
+                                cudaStream_t s) {
+  if ((int64_t)B * T == 0) return cudaSuccess;
+  seq_count_kernel<<<(B + 7) / 8, 256, 0, s>>>(B, T, lengths, mask, counts);
+  int64_t blocks = ((int64_t)B * T + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  loss_weight_kernel<<<(int)blocks, 256, 0, s>>>(B, T, G < 1 ? 1 : G, agg, tokens, seqs, groups, lengths, mask,
+                                                 counts, w);
+  g_launches.fetch_add(2, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_logits_backward(const void* logits, int32_t dtype, int64_t stride, int32_t V, int32_t B, int32_t T,
+                                   const int32_t* lengths, const int32_t* tokens, const float* lse, const float* dlogp,
+                                   const float* weight, void* grad, int32_t gdtype, int64_t gstride, int num_sms,
+                                   cudaStream_t s) {
+  const BwArgs a{logits, stride, V, B, T, lengths, tokens, lse, dlogp, weight, grad, gstride};
+  if (dtype == RLO_DTYPE_BF16)
+    return gdtype == RLO_DTYPE_BF16 ? launch_bw<__nv_bfloat16, __nv_bfloat16>(a, num_sms, s)
+                                    : launch_bw<__nv_bfloat16, float>(a, num_sms, s);
+  return gdtype == RLO_DTYPE_BF16 ? launch_bw<float, __nv_bfloat16>(a, num_sms, s)
+                                  : launch_bw<float, float>(a, num_sms, s);
+}
+
+}  // namespace rlo

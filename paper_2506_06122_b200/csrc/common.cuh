@@ -53,11 +53,12 @@ __device__ __forceinline__ f2 fadd2(f2 a, f2 b) {
 
 // 2^t for a pair on the FMA pipe (FA4-style MUFU offload): Cody-Waite split
 // t = j + f, j = rint(t) via the 1.5*2^23 magic add, f in [-0.5, 0.5];
-// degree-5 polynomial (relative error 1.9e-7 in fp32 Horner, on par with
-// MUFU.EX2's ~2 ulp); 2^j inserted into the exponent with one IMAD.
+// degree-5 (relative error 1.9e-7 in fp32 Horner, on par with MUFU.EX2's
+// ~2 ulp) or degree-4 polynomial; 2^j inserted into the exponent with one IMAD.
 // Inputs are clamped to >= -126 so the exponent add stays in the normal
 // range: t <= -126 yields 2^-126 (1.2e-38) instead of 0, which is below the
 // fp32 resolution of any sum it enters (s >= 1: it contains the max term).
+template <int DEG>  // 5: rel. err 1.9e-7; 4: 2.9e-6 (enough for 1e-5 on a sum whose offloaded share is <= 1/2)
 __device__ __forceinline__ f2 exp2_poly2(float tl, float th) {
   constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
   tl = fmaxf(tl, -126.0f);
@@ -66,10 +67,17 @@ __device__ __forceinline__ f2 exp2_poly2(float tl, float th) {
   const f2 r = fadd2(t, pk2(kMagic, kMagic));
   const f2 j = fadd2(r, pk2(-kMagic, -kMagic));
   const f2 f = ffma2(j, pk2(-1.0f, -1.0f), t);
-  f2 p = ffma2(f, pk2(0x1.5bba14p-10f, 0x1.5bba14p-10f), pk2(0x1.3cea88p-7f, 0x1.3cea88p-7f));
-  p = ffma2(p, f, pk2(0x1.c6b752p-5f, 0x1.c6b752p-5f));
-  p = ffma2(p, f, pk2(0x1.ebf9bcp-3f, 0x1.ebf9bcp-3f));
-  p = ffma2(p, f, pk2(0x1.62e42ap-1f, 0x1.62e42ap-1f));
+  f2 p;
+  if (DEG == 5) {
+    p = ffma2(f, pk2(0x1.5bba14p-10f, 0x1.5bba14p-10f), pk2(0x1.3cea88p-7f, 0x1.3cea88p-7f));
+    p = ffma2(p, f, pk2(0x1.c6b752p-5f, 0x1.c6b752p-5f));
+    p = ffma2(p, f, pk2(0x1.ebf9bcp-3f, 0x1.ebf9bcp-3f));
+    p = ffma2(p, f, pk2(0x1.62e42ap-1f, 0x1.62e42ap-1f));
+  } else {
+    p = ffma2(f, pk2(0x1.3a02ccp-7f, 0x1.3a02ccp-7f), pk2(0x1.c9fc46p-5f, 0x1.c9fc46p-5f));
+    p = ffma2(p, f, pk2(0x1.ec0378p-3f, 0x1.ec0378p-3f));
+    p = ffma2(p, f, pk2(0x1.62e12cp-1f, 0x1.62e12cp-1f));
+  }
   p = ffma2(p, f, pk2(1.0f, 1.0f));
   float pl, ph, rl, rh;
   upk2(p, pl, ph);

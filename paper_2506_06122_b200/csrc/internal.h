@@ -93,6 +93,7 @@ struct VocabArgs {
   float* o_ent;
   float* o_dlogp;
   float* o_loss;
+  float* o_lse;
   // scratch consumed by the per-sequence reduction
   float* s_loss;
   float* s_ratio;
@@ -132,6 +133,16 @@ cudaError_t launch_batch_reduce(const SeqRec* recs, int32_t nseq, int32_t G, dou
 cudaError_t launch_advantages(const AdvArgs& a, cudaStream_t s);
 cudaError_t launch_wstat_reduce(const WStat* w, int32_t n, double* out4, cudaStream_t s);
 cudaError_t launch_whiten_clip(const AdvArgs& a, const double* stats_all, int32_t world, cudaStream_t s);
+cudaError_t launch_loss_weights(int32_t B, int32_t T, int32_t G, int32_t agg, double tokens, double seqs,
+                                double groups, const int32_t* lengths, const uint8_t* mask, float* counts, float* w,
+                                cudaStream_t s);
+cudaError_t launch_logits_backward(const void* logits, int32_t dtype, int64_t stride, int32_t V, int32_t B, int32_t T,
+                                   const int32_t* lengths, const int32_t* tokens, const float* lse, const float* dlogp,
+                                   const float* weight, void* grad, int32_t gdtype, int64_t gstride, int num_sms,
+                                   cudaStream_t s);
+cudaError_t launch_value_loss(int32_t B, int32_t T, const int32_t* lengths, const uint8_t* mask, const float* values,
+                              const float* old_values, const float* returns, double clip, float* dv,
+                              double* seqsums, double* out4, cudaStream_t s);
 cudaError_t launch_synth_logits(void* dst, int32_t dtype, int64_t rows, int32_t V, int64_t row_stride,
                                 uint64_t seed, int32_t model_id, int64_t row_key_offset, cudaStream_t s);
 cudaError_t launch_synth_tokens(int32_t* dst, int64_t rows, int32_t V, uint64_t seed, int64_t row_key_offset,

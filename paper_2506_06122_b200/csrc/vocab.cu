@@ -31,26 +31,46 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
-template <typename ET, int U, bool ENT, int MATH>
+// PF: software prefetch — the next batch's U loads are issued before the
+// current batch's math, doubling the bytes in flight per thread.
+template <typename ET, int U, bool PF, bool ENT, int MATH>
 __device__ __forceinline__ void row_accumulate(const ET* __restrict__ row, int V, bool vec_ok, Acc& a) {
   using VT = Vec<ET>;
   using VV = typename VT::V;
+  constexpr int kStep = kThreads * U;
   const int tid = threadIdx.x;
   const int nvec = vec_ok ? V / VT::kElems : 0;
-  const int nfull = nvec / (kThreads * U) * (kThreads * U);
-  const VV* __restrict__ vrow = reinterpret_cast<const VV*>(row);
-  for (int base = 0; base < nfull; base += kThreads * U) {  // full batches: unpredicated loads
-    VV v[U];
+  const int nfull = nvec / kStep * kStep;
+  const VV* __restrict__ vrow = reinterpret_cast<const VV*>(row) + tid;
+  if (PF) {
+    if (nfull > 0) {
+      VV cur[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = ld_stream(vrow + base + u * kThreads + tid);
-    VT::template accumulate<U, ENT, MATH>(v, a);
+      for (int u = 0; u < U; ++u) cur[u] = ld_stream(vrow + u * kThreads);
+      for (int base = kStep; base < nfull; base += kStep) {
+        VV nxt[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) nxt[u] = ld_stream(vrow + base + u * kThreads);
+        VT::template accumulate<U, ENT, MATH>(cur, a);
+#pragma unroll
+        for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+      }
+      VT::template accumulate<U, ENT, MATH>(cur, a);
+    }
+  } else {
+    for (int base = 0; base < nfull; base += kStep) {  // full batches: unpredicated loads
+      VV v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld_stream(vrow + base + u * kThreads);
+      VT::template accumulate<U, ENT, MATH>(v, a);
+    }
   }
   if (nfull < nvec) {  // last partial batch
     VV v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int idx = nfull + u * kThreads + tid;
-      v[u] = idx < nvec ? ld_stream(vrow + idx) : VT::fill();
+      v[u] = idx < nvec ? ld_stream(vrow - tid + idx) : VT::fill();
     }
     VT::template accumulate<U, ENT, MATH>(v, a);
   }
@@ -65,7 +85,7 @@ __device__ __forceinline__ void row_accumulate(const ET* __restrict__ row, int V
   }
 }
 
-template <typename ET, int NT, int U, bool LOSS, bool ENT0, int MATH>
+template <typename ET, int NT, int U, bool PF, bool LOSS, bool ENT0, int MATH>
 __global__ void __launch_bounds__(kThreads) vocab_ldg_kernel(const VocabArgs a) {
   __shared__ float red[2][kWarps][NT][3];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -91,9 +111,9 @@ __global__ void __launch_bounds__(kThreads) vocab_ldg_kernel(const VocabArgs a) 
       acc_init(acc[k]);
       const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + row * a.stride[k];
       if (k == 0 && ENT0)
-        row_accumulate<ET, U, true, MATH>(rp, a.V, vec_ok, acc[k]);
+        row_accumulate<ET, U, PF, true, MATH>(rp, a.V, vec_ok, acc[k]);
       else
-        row_accumulate<ET, U, false, MATH>(rp, a.V, vec_ok, acc[k]);
+        row_accumulate<ET, U, PF, false, MATH>(rp, a.V, vec_ok, acc[k]);
     }
 #pragma unroll
     for (int k = 0; k < NT; ++k) {
@@ -113,10 +133,9 @@ __global__ void __launch_bounds__(kThreads) vocab_ldg_kernel(const VocabArgs a) 
   }
 }
 
-template <typename ET, int NT, bool LOSS, bool ENT0, int MATH>
+template <typename ET, int NT, bool LOSS, bool ENT0, int MATH, int U, bool PF>
 cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
-  constexpr int U = sizeof(ET) == 4 ? 8 : 4;
-  auto kern = vocab_ldg_kernel<ET, NT, U, LOSS, ENT0, MATH>;
+  auto kern = vocab_ldg_kernel<ET, NT, U, PF, LOSS, ENT0, MATH>;
   const int64_t nrows = (int64_t)a.B * a.T;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0);
@@ -143,22 +162,45 @@ bool use_tma(int esz) {
   return false;  // default: LDG streaming (measured faster than the TMA ring for fp32 and bf16, profiles/)
 }
 
+// LDG layout per dtype: fp32 U=8 (128 B in flight per thread); bf16 U=4
+// (64 B).  RLO_VOCAB_LDG selects the alternatives compiled for the hot bf16
+// fused-loss pass: 1 = U4 + prefetch, 2 = U8, 3 = U2 + prefetch.
+template <typename ET, int NT, bool LOSS, bool ENT0, int MATH>
+cudaError_t launch_ldg_layout(const VocabArgs& a, int num_sms, cudaStream_t s) {
+  if constexpr (sizeof(ET) == 2 && NT == 3 && LOSS) {
+    switch (env_int("RLO_VOCAB_LDG", 0)) {
+      case 1: return launch_ldg<ET, NT, LOSS, ENT0, MATH, 4, true>(a, num_sms, s);
+      case 2: return launch_ldg<ET, NT, LOSS, ENT0, MATH, 8, false>(a, num_sms, s);
+      case 3: return launch_ldg<ET, NT, LOSS, ENT0, MATH, 2, true>(a, num_sms, s);
+      default: break;
+    }
+  }
+  return launch_ldg<ET, NT, LOSS, ENT0, MATH, sizeof(ET) == 4 ? 8 : 4, false>(a, num_sms, s);
+}
+
 template <typename ET, int NT, bool LOSS, bool ENT0, int MATH>
 cudaError_t launch_impl(const VocabArgs& a, int num_sms, cudaStream_t s) {
   if (use_tma((int)sizeof(ET)) && tma_eligible(a, (int)sizeof(ET)))
     return launch_tma<ET, NT, LOSS, ENT0, MATH>(a, num_sms, s);
-  return launch_ldg<ET, NT, LOSS, ENT0, MATH>(a, num_sms, s);
+  return launch_ldg_layout<ET, NT, LOSS, ENT0, MATH>(a, num_sms, s);
 }
 
+// Instruction mix (vocab_common.cuh): fp32 {0, 1}, default 1; bf16 {1..5}, default 2.
 template <typename ET, int NT, bool LOSS, bool ENT0>
 cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
   if ((int64_t)a.B * a.T == 0) return cudaSuccess;
   const int math = env_int("RLO_VOCAB_MATH", sizeof(ET) == 2 ? 2 : 1);
-  switch (math) {
-    case 0: return launch_impl<ET, NT, LOSS, ENT0, 0>(a, num_sms, s);
-    case 2: return launch_impl<ET, NT, LOSS, ENT0, 2>(a, num_sms, s);
-    case 3: return launch_impl<ET, NT, LOSS, ENT0, 3>(a, num_sms, s);
-    default: return launch_impl<ET, NT, LOSS, ENT0, 1>(a, num_sms, s);
+  if constexpr (sizeof(ET) == 4) {
+    return math == 0 ? launch_impl<ET, NT, LOSS, ENT0, 0>(a, num_sms, s)
+                     : launch_impl<ET, NT, LOSS, ENT0, 1>(a, num_sms, s);
+  } else {
+    switch (math) {
+      case 1: return launch_impl<ET, NT, LOSS, ENT0, 1>(a, num_sms, s);
+      case 3: return launch_impl<ET, NT, LOSS, ENT0, 3>(a, num_sms, s);
+      case 4: return launch_impl<ET, NT, LOSS, ENT0, 4>(a, num_sms, s);
+      case 5: return launch_impl<ET, NT, LOSS, ENT0, 5>(a, num_sms, s);
+      default: return launch_impl<ET, NT, LOSS, ENT0, 2>(a, num_sms, s);
+    }
   }
 }
 

@@ -78,17 +78,23 @@ __device__ __forceinline__ void acc_warp_reduce(Acc& a) {
 //   0  scalar FFMA / MUFU.EX2 / FADD per element;
 //   1  packed: FFMA2 / FADD2 on element pairs, MUFU.EX2 per element;
 //   2  as 1, plus 1 of 4 element pairs of each non-entropy row through the
-//      FMA-pipe polynomial exp2 (exp2_poly2) instead of MUFU (25% offload);
-//   3  as 2 with 2 of 4 pairs (50% offload).
+//      FMA-pipe degree-5 polynomial exp2 (exp2_poly2) instead of MUFU (25%);
+//   3  as 2 with 2 of 4 pairs (50% offload);
+//   4, 5  as 2, 3 with the degree-4 polynomial (one FFMA2 fewer per pair).
 // The entropy (actor) row always uses MUFU: its 2^-126 floor would leak
 // into the entropy accumulator w.
 
+// MATH -> polynomial degree of the offloaded pairs (0: none) and whether half
+// (rather than a quarter) of the old/ref element pairs are offloaded.
+__host__ __device__ constexpr int poly_deg(int math) { return math == 2 || math == 3 ? 5 : math == 4 || math == 5 ? 4 : 0; }
+__host__ __device__ constexpr bool poly_half(int math) { return math == 3 || math == 5; }
+
 template <bool ENT>
-__device__ __forceinline__ void pair2(float zl, float zh, f2 L2, f2 nmL, f2& s, f2& w, bool poly) {
+__device__ __forceinline__ void pair2(float zl, float zh, f2 L2, f2 nmL, f2& s, f2& w, int poly) {
   const f2 t = ffma2(pk2(zl, zh), L2, nmL);
   float tl, th;
   upk2(t, tl, th);
-  const f2 e = poly ? exp2_poly2(tl, th) : pk2(ex2(tl), ex2(th));
+  const f2 e = poly == 5 ? exp2_poly2<5>(tl, th) : poly == 4 ? exp2_poly2<4>(tl, th) : pk2(ex2(tl), ex2(th));
   s = fadd2(s, e);
   if (ENT) w = ffma2(e, pk2(fmaxf(tl, kNegInit), fmaxf(th, kNegInit)), w);
 }
@@ -134,8 +140,8 @@ struct Vec<float> {
       f2 s0 = 0, s1 = 0, w0 = 0, w1 = 0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        pair2<ENT>(v[u].x, v[u].y, L2, nmL, s0, w0, false);
-        pair2<ENT>(v[u].z, v[u].w, L2, nmL, s1, w1, !ENT && MATH >= 2 && (u & 1));
+        pair2<ENT>(v[u].x, v[u].y, L2, nmL, s0, w0, 0);
+        pair2<ENT>(v[u].z, v[u].w, L2, nmL, s1, w1, (!ENT && (u & 1)) ? poly_deg(MATH) : 0);
       }
       a.s += hsum2(s0, s1);
       if (ENT) a.w += hsum2(w0, w1);
@@ -182,10 +188,10 @@ struct Vec<__nv_bfloat16> {
       f2 s0 = 0, s1 = 0, w0 = 0, w1 = 0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        pair2<ENT>(bf16lo(v[u].x), bf16hi(v[u].x), L2, nmL, s0, w0, false);
-        pair2<ENT>(bf16lo(v[u].y), bf16hi(v[u].y), L2, nmL, s1, w1, !ENT && MATH >= 2);
-        pair2<ENT>(bf16lo(v[u].z), bf16hi(v[u].z), L2, nmL, s0, w0, false);
-        pair2<ENT>(bf16lo(v[u].w), bf16hi(v[u].w), L2, nmL, s1, w1, !ENT && MATH >= 3);
+        pair2<ENT>(bf16lo(v[u].x), bf16hi(v[u].x), L2, nmL, s0, w0, 0);
+        pair2<ENT>(bf16lo(v[u].y), bf16hi(v[u].y), L2, nmL, s1, w1, ENT ? 0 : poly_deg(MATH));
+        pair2<ENT>(bf16lo(v[u].z), bf16hi(v[u].z), L2, nmL, s0, w0, 0);
+        pair2<ENT>(bf16lo(v[u].w), bf16hi(v[u].w), L2, nmL, s1, w1, (ENT || !poly_half(MATH)) ? 0 : poly_deg(MATH));
       }
       a.s += hsum2(s0, s1);
       if (ENT) a.w += hsum2(w0, w1);
@@ -220,7 +226,7 @@ __device__ __forceinline__ void flag_error(const VocabArgs& a, int code, int val
 
 // Loss epilogue for one loss-participating token (policy.cpp:355-374 + extensions), fp64.
 __device__ inline void loss_epilogue(const VocabArgs& a, int64_t row, double lp, double old, bool has_ref, double ref,
-                                     double ent) {
+                                     double ent, double lse) {
   const double A = (double)a.adv[row];
   const double eps = a.clip_eps;
   const double ratio = exp(lp - old);                       // policy.cpp:358
@@ -272,6 +278,7 @@ __device__ inline void loss_epilogue(const VocabArgs& a, int64_t row, double lp,
   if (a.o_ent) a.o_ent[row] = (float)ent;
   if (a.o_dlogp) a.o_dlogp[row] = (float)dlp;
   if (a.o_loss) a.o_loss[row] = (float)loss;
+  if (a.o_lse) a.o_lse[row] = (float)lse;
 }
 
 // Is `row` processed by this pass?  (forward_logprobs: every valid position;
@@ -302,6 +309,7 @@ __device__ __forceinline__ void write_inactive(const VocabArgs& a, int64_t row) 
     if (a.o_ent) a.o_ent[row] = 0.f;
     if (a.o_dlogp) a.o_dlogp[row] = 0.f;
     if (a.o_loss) a.o_loss[row] = 0.f;
+    if (a.o_lse) a.o_lse[row] = 0.f;
   }
 }
 
@@ -368,7 +376,7 @@ __device__ __forceinline__ void row_finish(const VocabArgs& a, const float (*red
     ref = (double)a.ref_lp_in[row];
     have_ref = true;
   }
-  loss_epilogue(a, row, lp[0], old, have_ref, ref, ent);
+  loss_epilogue(a, row, lp[0], old, have_ref, ref, ent, lse[0]);
 }
 
 }  // namespace vocab

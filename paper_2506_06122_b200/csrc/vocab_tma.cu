@@ -220,22 +220,27 @@ cudaError_t launch_tma(const VocabArgs& a, int num_sms, cudaStream_t s) {
 
 #define RLO_INST1(ET, NT, LOSS, ENT0, M) \
   template cudaError_t launch_tma<ET, NT, LOSS, ENT0, M>(const VocabArgs&, int, cudaStream_t);
-#define RLO_INST(ET, NT, LOSS, ENT0) \
-  RLO_INST1(ET, NT, LOSS, ENT0, 0)   \
-  RLO_INST1(ET, NT, LOSS, ENT0, 1)   \
-  RLO_INST1(ET, NT, LOSS, ENT0, 2)   \
-  RLO_INST1(ET, NT, LOSS, ENT0, 3)
-RLO_INST(float, 1, false, false)
-RLO_INST(float, 1, false, true)
-RLO_INST(__nv_bfloat16, 1, false, false)
-RLO_INST(__nv_bfloat16, 1, false, true)
-RLO_INST(float, 1, true, true)
-RLO_INST(float, 2, true, true)
-RLO_INST(float, 3, true, true)
-RLO_INST(__nv_bfloat16, 1, true, true)
-RLO_INST(__nv_bfloat16, 2, true, true)
-RLO_INST(__nv_bfloat16, 3, true, true)
-#undef RLO_INST
+#define RLO_INST_F(NT, LOSS, ENT0)         \
+  RLO_INST1(float, NT, LOSS, ENT0, 0)     \
+  RLO_INST1(float, NT, LOSS, ENT0, 1)
+#define RLO_INST_B(NT, LOSS, ENT0)                 \
+  RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 1)     \
+  RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 2)     \
+  RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 3)     \
+  RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 4)     \
+  RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 5)
+RLO_INST_F(1, false, false)
+RLO_INST_F(1, false, true)
+RLO_INST_F(1, true, true)
+RLO_INST_F(2, true, true)
+RLO_INST_F(3, true, true)
+RLO_INST_B(1, false, false)
+RLO_INST_B(1, false, true)
+RLO_INST_B(1, true, true)
+RLO_INST_B(2, true, true)
+RLO_INST_B(3, true, true)
+#undef RLO_INST_F
+#undef RLO_INST_B
 #undef RLO_INST1
 
 }  // namespace vocab

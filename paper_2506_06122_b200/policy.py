@@ -271,7 +271,7 @@ class Objective:
         """ppo_gradient loss part (policy.cpp:313-374), fused over the logits.
         Accumulates per-sequence sums until merge_gradients().  Returns the
         requested per-token outputs ([B,T] float32): logp, old_logp, ref_logp,
-        entropy, dlogp, loss."""
+        entropy, dlogp, loss, lse."""
         torch = _torch()
         B, T = tokens.shape
         _check_dev(tokens, torch.int32, "tokens")
@@ -281,7 +281,7 @@ class Objective:
             _check_dev(t, torch.float32, n)
         res = {k: torch.empty(B, T, dtype=torch.float32, device=tokens.device) for k in outputs}
         o = _abi.rlo_token_out()
-        for k in ("logp", "old_logp", "ref_logp", "entropy", "dlogp", "loss"):
+        for k in ("logp", "old_logp", "ref_logp", "entropy", "dlogp", "loss", "lse"):
             setattr(o, k, res[k].data_ptr() if k in res else None)
         L_old, L_ref = _logits(old_logits, "old_logits"), _logits(ref_logits, "ref_logits")
         check(_abi.lib().rlo_ppo_gradient(
@@ -299,6 +299,43 @@ class Objective:
                                              _stream(stream, self.device)))
         stats = UpdateStats.from_c(st)
         return (stats, np.array(part.v[:])) if with_partials else stats
+
+    # -- next rows: backward epilogue, critic ----------------------------------
+    def loss_weights(self, cfg: TrainConfig, lengths, stats: "UpdateStats", T, mask=None, stream=None):
+        """d(L)/d(loss_t) per token under cfg.loss_agg with the merged counts."""
+        torch = _torch()
+        st = _abi.rlo_stats()
+        for f in fields(UpdateStats):
+            setattr(st, f.name, getattr(stats, f.name))
+        w = torch.empty(int(lengths.numel()), T, dtype=torch.float32, device=lengths.device)
+        check(_abi.lib().rlo_loss_weights(self._h, C.byref(cfg.to_c()), C.byref(_batch(lengths, None, mask, T)),
+                                          C.byref(st), _ptr(w), _stream(stream, self.device)))
+        return w
+
+    def logits_backward(self, tokens, lengths, logits, lse, dlogp, weight, grad=None, grad_dtype=None, stream=None):
+        """Actor backward epilogue (policy.cpp:375-379): dL/dlogits rows
+        w*dlogp*(onehot - softmax); returns the gradient tensor."""
+        torch = _torch()
+        B, T = tokens.shape
+        if grad is None:
+            grad = torch.empty(B * T, logits.shape[-1], dtype=grad_dtype or logits.dtype, device=logits.device)
+        G = _logits(grad, "grad")
+        check(_abi.lib().rlo_logits_backward(
+            self._h, C.byref(_batch(lengths, tokens, None, T)), C.byref(_logits(logits)), _ptr(lse), _ptr(dlogp),
+            _ptr(weight), C.c_void_p(grad.data_ptr()), G.dtype, G.row_stride, _stream(stream, self.device)))
+        return grad
+
+    def value_loss(self, lengths, values, returns, old_values=None, value_clip=0.0, mask=None, dvalue=True,
+                   stream=None):
+        """Critic value loss (value_gradient, policy.cpp:474-540); returns (stats dict, dvalue)."""
+        torch = _torch()
+        B, T = values.shape
+        dv = torch.empty_like(values) if dvalue else None
+        st = _abi.rlo_value_stats()
+        check(_abi.lib().rlo_value_loss(self._h, C.byref(_batch(lengths, None, mask, T)), _ptr(values),
+                                        _ptr(old_values), _ptr(returns), C.c_double(value_clip), _ptr(dv),
+                                        C.byref(st), _stream(stream, self.device)))
+        return {k: getattr(st, k) for k, _ in st._fields_}, dv
 
     def rank_partials(self, cfg: TrainConfig, stream=None) -> np.ndarray:
         """This rank's GradAccum scalars (no cross-rank merge, no checks); resets."""

@@ -136,9 +136,11 @@ def ppo_cases(rng):
         kw = dict(clip_eps=float(rng.choice([0.1, 0.2, 0.3])), kl_coef=float(rng.choice([0.0, 0.1])))
         world = int(rng.choice([1, 2, 3]))
         st = O.ref_ppo_stats_b2(row, B, T, lengths, tokens, mask, old, ref_lp, adv, O.TrainConfig(**kw), world)
+        # merged gradient w.r.t. the shared logits row (policy.cpp:375-379, :391, :439-440)
+        grad = O.ref_ppo_grad_b2(row, B, T, lengths, tokens, mask, old, ref_lp, adv, O.TrainConfig(**kw), world)
         cases.append(dict(cfg=kw, V=V, B=B, T=T, world=world, row=row.tolist(), lengths=lengths.tolist(),
                           tokens=tokens.tolist(), mask=None if mask is None else mask.tolist(), old=old.tolist(),
-                          ref=ref_lp.tolist(), adv=adv.tolist(), ref_stats=st))
+                          ref=ref_lp.tolist(), adv=adv.tolist(), ref_stats=st, ref_grad_row=grad.tolist()))
     # clipped-branch KAT (test_policy.cpp:357-379): ratio=e^1 >> 1.2, A=2 -> loss -2.4
     V = 9
     row = rng.standard_normal(V)
@@ -157,6 +159,23 @@ def ppo_cases(rng):
     with open(os.path.join(HERE, "ppo_stats.json"), "w") as f:
         json.dump({"source": "ppo_gradient+merge_gradients policy.cpp:313-450 (b2 trick)", "cases": cases,
                    "errors": errors}, f)
+
+
+def value_cases(rng):
+    """value_gradient (policy.cpp:474-540): every position's value = vb (value-head bias)."""
+    cases = []
+    for k in range(5):
+        B, T = int(rng.integers(2, 7)), int(rng.integers(2, 12))
+        lengths = rng.integers(0, T + 1, B).astype(np.int32)
+        lengths[0] = T
+        mask = (rng.random(B * T) < 0.75).astype(np.uint8) if k % 2 else None
+        targets = rng.standard_normal(B * T) * 2.0
+        vb = float(rng.standard_normal())
+        r = O.ref_value_loss_b2(vb, B, T, lengths, mask, targets)
+        cases.append(dict(B=B, T=T, vb=vb, lengths=lengths.tolist(), mask=None if mask is None else mask.tolist(),
+                          targets=targets.tolist(), ref=r))
+    with open(os.path.join(HERE, "value_loss.json"), "w") as f:
+        json.dump({"source": "value_gradient policy.cpp:474-540 (value = vb everywhere)", "cases": cases}, f)
 
 
 def config_cases():
@@ -180,6 +199,7 @@ def main():
     extra = forward_logprobs_case(rng)
     advantage_cases(rng)
     ppo_cases(rng)
+    value_cases(np.random.default_rng(474))
     cfgs, splits = config_cases()
     with open(os.path.join(HERE, "misc.json"), "w") as f:
         json.dump({"train_config_validate": cfgs, "split_sizes": splits, **extra}, f, indent=1)

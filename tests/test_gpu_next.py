@@ -1,0 +1,120 @@
+"""GPU parity of the §8f "next" rows: aggregation weights, the actor backward
+epilogue (dlogits) and the critic value loss, against the reference's own
+gradients (golden) and the oracle."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+G = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _load(n):
+    with open(os.path.join(G, n)) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+
+    import paper_2506_06122_b200 as rlo
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch, rlo, rlo.Objective(0)
+
+
+def dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def test_backward_matches_reference_gradient(env):
+    """Sum over rows of dlogits == the reference's merged d(loss)/d(b2) (b2 trick)."""
+    torch, rlo, obj = env
+    for c in _load("ppo_stats.json")["cases"]:
+        if "ref_grad_row" not in c:
+            continue
+        B, T, V = c["B"], c["T"], c["V"]
+        cfg = rlo.TrainConfig(**c["cfg"])
+        logits = dev(torch, np.tile(np.asarray(c["row"], np.float32), (B * T, 1)))
+        toks = dev(torch, np.asarray(c["tokens"], np.int32).reshape(B, T))
+        lengths = dev(torch, np.asarray(c["lengths"], np.int32))
+        mask = None if c["mask"] is None else dev(torch, np.asarray(c["mask"], np.uint8).reshape(B, T))
+        f = lambda k: None if c[k] is None else dev(torch, np.asarray(c[k], np.float32).reshape(B, T))  # noqa: E731
+        outs = obj.ppo_gradient(cfg, toks, lengths, logits, f("adv"), mask=mask, old_logprobs=f("old"),
+                                ref_logprobs=f("ref"), outputs=("dlogp", "lse"))
+        st = obj.merge_gradients(cfg)
+        w = obj.loss_weights(cfg, lengths, st, T, mask=mask)
+        grad = obj.logits_backward(toks, lengths, logits, outs["lse"], outs["dlogp"], w, grad_dtype=torch.float32)
+        g = grad.double().sum(0).cpu().numpy()
+        ref = np.asarray(c["ref_grad_row"])
+        assert np.max(np.abs(g - ref)) <= 2e-5 * max(1.0, np.abs(ref).max()), (np.abs(g - ref).max(), c["cfg"])
+
+
+@pytest.mark.parametrize("dt,gdt", [("f32", "f32"), ("bf16", "bf16"), ("bf16", "f32")])
+@pytest.mark.parametrize("agg", [0, 1, 3])
+def test_backward_rows_vs_oracle(env, dt, gdt, agg):
+    torch, rlo, obj = env
+    rng = np.random.default_rng(agg)
+    B, T, V = 6, 8, 4099 if dt == "f32" else 4096  # odd V exercises the scalar tail
+    tdt = torch.float32 if dt == "f32" else torch.bfloat16
+    gtdt = torch.float32 if gdt == "f32" else torch.bfloat16
+    x = (torch.randn(B * T, V, generator=torch.Generator().manual_seed(agg)) * 3).to(tdt).cuda()
+    lengths = rng.integers(1, T + 1, B).astype(np.int32)
+    mask = (rng.random((B, T)) < 0.8).astype(np.uint8)
+    toks = rng.integers(0, V, (B, T)).astype(np.int32)
+    adv = rng.uniform(-1, 1, (B, T)).astype(np.float32)
+    old = rng.uniform(-12, -4, (B, T)).astype(np.float32)
+    cfg = rlo.TrainConfig(loss_agg=agg, group_size=3)
+    outs = obj.ppo_gradient(cfg, dev(torch, toks), dev(torch, lengths), x, dev(torch, adv), mask=dev(torch, mask),
+                            old_logprobs=dev(torch, old), outputs=("dlogp", "lse"))
+    st = obj.merge_gradients(cfg)
+    w = obj.loss_weights(cfg, dev(torch, lengths), st, T, mask=dev(torch, mask))
+    ow = O.loss_weights(O.TrainConfig(loss_agg=agg, group_size=3), B, T, lengths, mask)
+    np.testing.assert_allclose(w.cpu().numpy().ravel(), ow, rtol=1e-6, atol=0)
+    grad = obj.logits_backward(dev(torch, toks), dev(torch, lengths), x, outs["lse"], outs["dlogp"], w,
+                               grad_dtype=gtdt).float().cpu().numpy()
+    rows = x.float().cpu().numpy()
+    dl = outs["dlogp"].cpu().numpy().ravel()
+    tol = 1e-5 if gdt == "f32" else 8e-3  # bf16 output: 8-bit mantissa
+    for i in range(B * T):
+        scale = float(ow[i] * dl[i])
+        want = O.logits_backward_row(rows[i].astype(np.float64), int(toks.ravel()[i]), scale) if scale else np.zeros(V)
+        err = np.abs(grad[i] - want).max()
+        assert err <= tol * max(abs(scale), 1e-30) + 1e-12, (i, err, scale)
+
+
+def test_value_loss_matches_reference(env):
+    torch, rlo, obj = env
+    for c in _load("value_loss.json")["cases"]:
+        B, T = c["B"], c["T"]
+        mask = None if c["mask"] is None else dev(torch, np.asarray(c["mask"], np.uint8).reshape(B, T))
+        vals = dev(torch, np.full((B, T), c["vb"], np.float32))
+        st, dv = obj.value_loss(dev(torch, np.asarray(c["lengths"], np.int32)), vals,
+                                dev(torch, np.asarray(c["targets"], np.float32).reshape(B, T)), mask=mask)
+        r = c["ref"]
+        assert st["tokens"] == r["tokens"]
+        assert abs(st["loss"] * st["tokens"] - r["loss_sum"]) <= 1e-5 * max(1.0, abs(r["loss_sum"]))
+        assert abs(float(dv.double().sum()) - r["grad_vb"]) <= 1e-5 * max(1.0, abs(r["grad_vb"]))
+
+
+def test_clipped_value_loss_vs_oracle(env):
+    torch, rlo, obj = env
+    rng = np.random.default_rng(5)
+    B, T = 16, 33
+    lengths = rng.integers(0, T + 1, B).astype(np.int32)
+    lengths[0] = T
+    mask = (rng.random((B, T)) < 0.9).astype(np.uint8)
+    v = rng.standard_normal((B, T)).astype(np.float32)
+    vo = (v + rng.standard_normal((B, T)) * 0.3).astype(np.float32)
+    R = rng.standard_normal((B, T)).astype(np.float32)
+    st, dv = obj.value_loss(dev(torch, lengths), dev(torch, v), dev(torch, R), old_values=dev(torch, vo),
+                            value_clip=0.2, mask=dev(torch, mask))
+    odv, o = O.value_loss(B, T, lengths, mask, v, vo, R, 0.2)
+    assert st["tokens"] == o["tokens"] and st["clip_fraction"] * st["tokens"] == o["clipped"]
+    assert abs(st["loss"] - o["loss_sum"] / o["tokens"]) <= 1e-6
+    np.testing.assert_allclose(dv.cpu().numpy().ravel(), odv, rtol=1e-5, atol=1e-6)
