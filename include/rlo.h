@@ -319,6 +319,21 @@ rlo_status rlo_value_loss(rlo_handle* h, const rlo_batch* batch, const float* va
                           const float* returns, double value_clip, float* out_dvalue, rlo_value_stats* out,
                           void* stream);
 
+/* Sampling-time log-probs: decode_next (policy.cpp:143-169) for n_rows logits
+ * rows — a tempered categorical draw by a CDF walk in token order with the
+ * reference's keyed uniform u = keyed_double({seed, version, sample_key[i],
+ * position[i]}) (rng.hpp:82-85), returning the token and its UNtempered
+ * log-prob (policy.cpp:168), i.e. response_logprobs, so the PPO ratio needs
+ * no separate old-policy logits pass.  fp64 internally, like the reference.
+ * sample_keys / positions [n_rows] device uint64; out_tokens int32 [n_rows];
+ * out_logp float [n_rows].  ConfigError for temperature <= 0 (policy.cpp:146). */
+rlo_status rlo_decode_sample(rlo_handle* h, const rlo_logits* logits, int32_t n_rows, double temperature,
+                             uint64_t seed, uint64_t version, const uint64_t* sample_keys, const uint64_t* positions,
+                             int32_t* out_tokens, float* out_logp, void* stream);
+
+/* rng::hash_str (rng.hpp:34-41): the per-sample key of a sample_id. Host only. */
+uint64_t rlo_sample_key(const char* sample_id);
+
 /* Synchronise `stream` and report device-side input errors (OOV tokens). */
 rlo_status rlo_sync(rlo_handle* h, void* stream);
 

@@ -336,3 +336,34 @@ def ref_value_loss_b2(vb, B, T, lengths, mask, targets):
                                    _p(targets), _p(out), err, C.c_int32(512))
     _check(code, err)
     return dict(zip(["loss_sum", "tokens", "grad_vb"], out.tolist()))
+
+
+# ---- decode_next (sampling-time log-probs) ------------------------------------
+
+def decode_next(z, temperature, seed, version, sample_key, position):
+    z = _f64(z)
+    lp = C.c_double()
+    tok = lib().orc_decode_next(_p(z), C.c_int32(z.size), C.c_double(temperature), C.c_uint64(seed),
+                                C.c_uint64(version), C.c_uint64(sample_key), C.c_uint64(position), C.byref(lp))
+    return int(tok), lp.value
+
+
+def hash_str(s):
+    lib().orc_hash_str.restype = C.c_uint64
+    return int(lib().orc_hash_str(s.encode()))
+
+
+def ref_decode_b2(row, temperature, seed, version, sample_key, position):
+    row = _f64(row)
+    tok, lp = C.c_int32(), C.c_double()
+    err = C.create_string_buffer(512)
+    code = ref().ref_decode_b2(_p(row), C.c_int32(row.size), C.c_double(temperature), C.c_uint64(seed),
+                               C.c_uint64(version), C.c_uint64(sample_key), C.c_uint64(position), C.byref(tok),
+                               C.byref(lp), err, C.c_int32(512))
+    _check(code, err)
+    return tok.value, lp.value
+
+
+def ref_hash_str(s):
+    ref().ref_hash_str.restype = C.c_uint64
+    return int(ref().ref_hash_str(s.encode()))

@@ -432,6 +432,58 @@ void orc_value_loss(int32_t B, int32_t T, const int32_t* lengths, const uint8_t*
   out4[3] = vsum;
 }
 
+/* ---- decode_next: policy.cpp:143-169 --------------------------------------- */
+static uint64_t orc_splitmix(uint64_t* state) { /* rng.hpp:15-20 */
+  uint64_t z = (*state += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+int32_t orc_decode_next(const double* z, int32_t V, double temperature, uint64_t seed, uint64_t version,
+                        uint64_t sample_key, uint64_t position, double* logp) {
+  double m = z[0];
+  for (int32_t v = 1; v < V; ++v) m = (m < z[v]) ? z[v] : m; /* :151-152 */
+  double* probs = (double*)malloc(sizeof(double) * (size_t)V);
+  double total = 0.0;
+  for (int32_t v = 0; v < V; ++v) { /* :153-157 */
+    probs[v] = exp((z[v] - m) / temperature);
+    total += probs[v];
+  }
+  /* keyed_double({seed, version, sample_key, position}), rng.hpp:23-31, 83-85 */
+  uint64_t state = 0x2545f4914f6cdd1dULL;
+  uint64_t h = orc_splitmix(&state);
+  const uint64_t keys[4] = {seed, version, sample_key, position};
+  for (int k = 0; k < 4; ++k) {
+    state ^= keys[k];
+    h ^= orc_splitmix(&state);
+  }
+  const double u = (double)(h >> 11) * 0x1.0p-53;
+  double acc = 0.0;
+  int32_t chosen = V - 1; /* :159-167 */
+  for (int32_t v = 0; v < V; ++v) {
+    acc += probs[v] / total;
+    if (u < acc) {
+      chosen = v;
+      break;
+    }
+  }
+  free(probs);
+  double lse;
+  orc_logsoftmax_row(z, V, &lse, NULL);
+  *logp = z[chosen] - lse; /* :168, untempered */
+  return chosen;
+}
+
+uint64_t orc_hash_str(const char* s) { /* rng.hpp:34-41 */
+  uint64_t h = 0xcbf29ce484222325ULL;
+  for (const unsigned char* c = (const unsigned char*)s; *c; ++c) {
+    h ^= *c;
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}
+
 /* ---- synthetic inputs (include/rlo_synth.h) -------------------------------- */
 static void synth_row_f(float* out, int32_t V, uint64_t seed, int32_t model, uint64_t row_key) {
   int32_t spikes[RLO_SYNTH_SPIKES];

@@ -83,6 +83,13 @@ void orc_value_loss(int32_t B, int32_t T, const int32_t* lengths, const uint8_t*
                     const double* old_values, const double* returns, double value_clip, double* out_dv,
                     double* out4);
 
+/* decode_next restated (policy.cpp:143-169) on one logits row: tempered CDF
+ * walk with u = keyed_double({seed, version, sample_key, position})
+ * (rng.hpp:15-31, 82-85); returns the token, *logp = untempered log-prob. */
+int32_t orc_decode_next(const double* z, int32_t V, double temperature, uint64_t seed, uint64_t version,
+                        uint64_t sample_key, uint64_t position, double* logp);
+uint64_t orc_hash_str(const char* s); /* rng.hpp:34-41 */
+
 /* Synthetic row / token of include/rlo_synth.h, as doubles (bf16-rounded
  * when dtype is bf16). */
 void orc_synth_row(double* out, int32_t dtype, int32_t V, uint64_t seed, int32_t model, uint64_t row_key);

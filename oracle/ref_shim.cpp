@@ -23,6 +23,7 @@
 
 #include "rollmini/errors.hpp"
 #include "rollmini/policy.hpp"
+#include "rollmini/rng.hpp"
 #include "rollmini/sample.hpp"
 
 extern "C" {
@@ -207,6 +208,27 @@ int32_t ref_value_loss_b2(double vb, int32_t B, int32_t T, const int32_t* length
     out3[2] = acc.grad[p.layout.off_vb()];
   });
 }
+
+// decode_next itself (policy.cpp:143-169) on an arbitrary row (b2 trick),
+// with params.version = `version`.
+int32_t ref_decode_b2(const double* row, int32_t V, double temperature, uint64_t seed, uint64_t version,
+                      uint64_t sample_key, uint64_t position, int32_t* out_tok, double* out_lp, char* err,
+                      int32_t errlen) {
+  return guarded(err, errlen, [&] {
+    PolicyParams p = b2_params(V);
+    p.version = version;
+    std::memcpy(p.values.data() + p.layout.off_b2(), row, sizeof(double) * V);
+    PolicyWorkspace ws;
+    ws.resize(p.layout);
+    const int ctx[1] = {0};
+    DecodeStep ds = decode_next(p, std::span<const int>(ctx, 1), temperature, seed, sample_key,
+                                static_cast<size_t>(position), kWindowPadToken, ws);
+    *out_tok = ds.token;
+    *out_lp = ds.logprob;
+  });
+}
+
+uint64_t ref_hash_str(const char* s) { return rng::hash_str(s); }
 
 // merge_gradients (policy.cpp:421-450) on scalar partials with empty grads.
 int32_t ref_merge_scalars(const double* parts5, int32_t nranks, double* out5, char* err, int32_t errlen) {

@@ -8,10 +8,11 @@ from ._abi import LIB_PATH, declared_symbols  # noqa: F401
 from .errors import (CollectError, ConfigError, CudaError, DispatchError, Error, InputError,  # noqa: F401
                      TrainingError)
 from .policy import (Message, Objective, PolicyWorker, TrainConfig, UpdateStats, launch_count,  # noqa: F401
-                     merge_partials, shard_plan, split_sizes, synth_logits, synth_tokens, whiten_combine)
+                     merge_partials, sample_key, shard_plan, split_sizes, synth_logits, synth_tokens,
+                     whiten_combine)
 
 __all__ = [
     "Objective", "PolicyWorker", "Message", "TrainConfig", "UpdateStats", "split_sizes", "shard_plan",
-    "merge_partials", "whiten_combine", "launch_count", "synth_logits", "synth_tokens", "Error", "ConfigError", "InputError",
+    "merge_partials", "whiten_combine", "sample_key", "launch_count", "synth_logits", "synth_tokens", "Error", "ConfigError", "InputError",
     "TrainingError", "DispatchError", "CollectError", "CudaError",
 ]

@@ -798,6 +798,31 @@ rlo_status rlo_value_loss(rlo_handle* h, const rlo_batch* batch, const float* va
   return RLO_OK;
 }
 
+rlo_status rlo_decode_sample(rlo_handle* h, const rlo_logits* logits, int32_t n_rows, double temperature,
+                             uint64_t seed, uint64_t version, const uint64_t* sample_keys, const uint64_t* positions,
+                             int32_t* out_tokens, float* out_logp, void* stream) {
+  if (!h) return fail(RLO_ERR_INPUT, "decode: null handle");
+  if (!(temperature > 0.0)) return fail(RLO_ERR_CONFIG, "decode: temperature must be positive");  // policy.cpp:146
+  if (n_rows < 0) return fail(RLO_ERR_INPUT, "decode: negative row count");
+  if (n_rows == 0) return RLO_OK;
+  RLO_TRY(check_logits(logits, "decode", "policy"));
+  if (!sample_keys || !positions || !out_tokens || !out_logp)
+    return fail(RLO_ERR_INPUT, "decode: sample_keys, positions, out_tokens and out_logp are required");
+  DeviceGuard g(h->device);
+  RLO_CUDA(launch_decode(logits->data, logits->dtype, logits->row_stride, logits->V, n_rows, temperature, seed, version,
+                         sample_keys, positions, out_tokens, out_logp, h->num_sms, static_cast<cudaStream_t>(stream)));
+  return RLO_OK;
+}
+
+uint64_t rlo_sample_key(const char* sample_id) {  // rng::hash_str, FNV-1a 64
+  uint64_t hsh = 0xcbf29ce484222325ULL;
+  for (const unsigned char* c = reinterpret_cast<const unsigned char*>(sample_id); c && *c; ++c) {
+    hsh ^= *c;
+    hsh *= 0x100000001b3ULL;
+  }
+  return hsh;
+}
+
 rlo_status rlo_synth_logits(void* dst, int32_t dtype, int64_t rows, int32_t V, int64_t row_stride, uint64_t seed,
                             int32_t model_id, int64_t row_key_offset, void* stream) {
   if (!dst && rows > 0) return fail(RLO_ERR_INPUT, "synth_logits: null destination");

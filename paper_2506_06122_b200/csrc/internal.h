@@ -143,6 +143,9 @@ cudaError_t launch_logits_backward(const void* logits, int32_t dtype, int64_t st
 cudaError_t launch_value_loss(int32_t B, int32_t T, const int32_t* lengths, const uint8_t* mask, const float* values,
                               const float* old_values, const float* returns, double clip, float* dv,
                               double* seqsums, double* out4, cudaStream_t s);
+cudaError_t launch_decode(const void* logits, int32_t dtype, int64_t stride, int32_t V, int32_t n, double temperature,
+                          uint64_t seed, uint64_t version, const uint64_t* keys, const uint64_t* positions,
+                          int32_t* out_tok, float* out_lp, int num_sms, cudaStream_t s);
 cudaError_t launch_synth_logits(void* dst, int32_t dtype, int64_t rows, int32_t V, int64_t row_stride,
                                 uint64_t seed, int32_t model_id, int64_t row_key_offset, cudaStream_t s);
 cudaError_t launch_synth_tokens(int32_t* dst, int64_t rows, int32_t V, uint64_t seed, int64_t row_key_offset,

@@ -185,11 +185,11 @@ cudaError_t launch_impl(const VocabArgs& a, int num_sms, cudaStream_t s) {
   return launch_ldg_layout<ET, NT, LOSS, ENT0, MATH>(a, num_sms, s);
 }
 
-// Instruction mix (vocab_common.cuh): fp32 {0, 1}, default 1; bf16 {1..5}, default 2.
+// Instruction mix (vocab_common.cuh): fp32 {0, 1}, default 1; bf16 {1..5}, default 4 (profiles/r1_vocab_sweep.txt).
 template <typename ET, int NT, bool LOSS, bool ENT0>
 cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
   if ((int64_t)a.B * a.T == 0) return cudaSuccess;
-  const int math = env_int("RLO_VOCAB_MATH", sizeof(ET) == 2 ? 2 : 1);
+  const int math = env_int("RLO_VOCAB_MATH", sizeof(ET) == 2 ? 4 : 1);
   if constexpr (sizeof(ET) == 4) {
     return math == 0 ? launch_impl<ET, NT, LOSS, ENT0, 0>(a, num_sms, s)
                      : launch_impl<ET, NT, LOSS, ENT0, 1>(a, num_sms, s);

@@ -337,6 +337,19 @@ class Objective:
                                         C.byref(st), _stream(stream, self.device)))
         return {k: getattr(st, k) for k, _ in st._fields_}, dv
 
+    def decode_sample(self, logits, temperature, seed, version, sample_keys, positions, stream=None):
+        """decode_next (policy.cpp:143-169) per row: (tokens int32, untempered logp float32)."""
+        torch = _torch()
+        n = logits.numel() // logits.shape[-1]
+        _check_dev(sample_keys, torch.int64, "sample_keys")
+        _check_dev(positions, torch.int64, "positions")
+        tok = torch.empty(n, dtype=torch.int32, device=logits.device)
+        lp = torch.empty(n, dtype=torch.float32, device=logits.device)
+        check(_abi.lib().rlo_decode_sample(self._h, C.byref(_logits(logits)), n, C.c_double(temperature),
+                                           C.c_uint64(seed), C.c_uint64(version), _ptr(sample_keys), _ptr(positions),
+                                           _ptr(tok), _ptr(lp), _stream(stream, self.device)))
+        return tok, lp
+
     def rank_partials(self, cfg: TrainConfig, stream=None) -> np.ndarray:
         """This rank's GradAccum scalars (no cross-rank merge, no checks); resets."""
         part = _abi.rlo_partials()
@@ -438,3 +451,8 @@ class PolicyWorker:
             out.scalars = {"loss_sum": p[0], "ratio_sum": p[1], "kl_sum": p[2], "clipped": p[4], "tokens": p[6]}
             return out
         raise DispatchError(f"policy worker: unimplemented method '{method}'")
+
+
+def sample_key(sample_id: str) -> int:
+    """rng::hash_str (rng.hpp:34-41): the per-sample key decode_next draws with."""
+    return int(_abi.lib().rlo_sample_key(sample_id.encode()))

@@ -178,6 +178,28 @@ def value_cases(rng):
         json.dump({"source": "value_gradient policy.cpp:474-540 (value = vb everywhere)", "cases": cases}, f)
 
 
+def decode_cases(rng):
+    """decode_next (policy.cpp:143-169) through the reference's own code (b2 trick)."""
+    cases = []
+    rows = []
+    for k in range(12):
+        V = int(rng.choice([9, 52, 1000, 2053]))
+        scale = float(rng.choice([0.5, 2.0, 4.0]))
+        row = (rng.standard_normal(V) * scale).astype(np.float32).astype(np.float64)
+        for _ in range(16):
+            T = float(rng.choice([0.3, 0.7, 1.0, 1.5]))
+            seed, version = int(rng.integers(0, 2**63)), int(rng.integers(1, 50))
+            sid = f"s{int(rng.integers(0, 10**6))}"
+            key, pos = O.ref_hash_str(sid), int(rng.integers(0, 4096))
+            tok, lp = O.ref_decode_b2(row, T, seed, version, key, pos)
+            cases.append(dict(row=len(rows), temperature=T, seed=seed, version=version, sample_id=sid, sample_key=key,
+                              position=pos, ref_token=tok, ref_logp=lp))
+        rows.append(row.tolist())
+    with open(os.path.join(HERE, "decode.json"), "w") as f:
+        json.dump({"source": "decode_next policy.cpp:143-169 (b2 trick), hash_str rng.hpp:34-41", "rows": rows,
+                   "cases": cases}, f)
+
+
 def config_cases():
     """TrainConfig::validate messages (policy.cpp:29-37) and split_sizes (sample.cpp:99-105)."""
     bad = [dict(clip_eps=0.0), dict(clip_eps=1.0), dict(kl_coef=-0.1), dict(learning_rate=-1.0),
@@ -200,6 +222,7 @@ def main():
     advantage_cases(rng)
     ppo_cases(rng)
     value_cases(np.random.default_rng(474))
+    decode_cases(np.random.default_rng(143))
     cfgs, splits = config_cases()
     with open(os.path.join(HERE, "misc.json"), "w") as f:
         json.dump({"train_config_validate": cfgs, "split_sizes": splits, **extra}, f, indent=1)

@@ -118,3 +118,50 @@ def test_clipped_value_loss_vs_oracle(env):
     assert st["tokens"] == o["tokens"] and st["clip_fraction"] * st["tokens"] == o["clipped"]
     assert abs(st["loss"] - o["loss_sum"] / o["tokens"]) <= 1e-6
     np.testing.assert_allclose(dv.cpu().numpy().ravel(), odv, rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_decode_sample_matches_reference(env, dt):
+    """Tokens bit-exact with the reference's decode_next draws; untempered logp within 1e-5."""
+    torch, rlo, obj = env
+    d = _load("decode.json")
+    tdt = torch.float32 if dt == "f32" else torch.bfloat16
+    by_row = {}
+    for c in d["cases"]:
+        by_row.setdefault(c["row"], []).append(c)
+    for r, cases in by_row.items():
+        row = np.asarray(d["rows"][r], np.float32)
+        if dt == "bf16":
+            row = torch.from_numpy(row).to(torch.bfloat16).float().numpy()
+        x = torch.from_numpy(np.tile(row, (len(cases), 1))).to(tdt).cuda()
+        for temp in sorted({c["temperature"] for c in cases}):
+            sub = [c for c in cases if c["temperature"] == temp]
+            for c in sub:  # one launch per (seed, version) pair: they are kernel-wide arguments
+                keys = dev(torch, np.array([c["sample_key"]], dtype=np.uint64).view(np.int64))
+                pos = dev(torch, np.array([c["position"]], dtype=np.int64))
+                tok, lp = obj.decode_sample(x[:1], temp, c["seed"], c["version"], keys, pos)
+                want_tok, want_lp = (c["ref_token"], c["ref_logp"]) if dt == "f32" else \
+                    O.decode_next(row.astype(np.float64), temp, c["seed"], c["version"], c["sample_key"], c["position"])
+                assert int(tok.item()) == want_tok, (r, temp, c["position"])
+                assert abs(float(lp.item()) - want_lp) <= 1e-5 * max(1.0, abs(want_lp))
+
+
+def test_decode_sample_batch_and_distribution(env):
+    """Many rows in one launch (keys / positions vary per row) == the oracle, and the
+    empirical token frequencies follow the tempered softmax."""
+    torch, rlo, obj = env
+    rng = np.random.default_rng(9)
+    V, n, temp = 257, 4096, 0.8
+    row = rng.standard_normal(V).astype(np.float32) * 2
+    x = torch.from_numpy(np.tile(row, (n, 1))).cuda()
+    keys = rng.integers(0, 2**62, n).astype(np.int64)
+    pos = np.arange(n, dtype=np.int64)
+    tok, lp = obj.decode_sample(x, temp, 1234, 7, dev(torch, keys), dev(torch, pos))
+    tok = tok.cpu().numpy()
+    for i in range(0, n, 97):
+        want, _ = O.decode_next(row.astype(np.float64), temp, 1234, 7, int(keys[i]), int(pos[i]))
+        assert tok[i] == want
+    p = np.exp((row - row.max()) / temp)
+    p /= p.sum()
+    freq = np.bincount(tok, minlength=V) / n
+    assert np.abs(freq - p).max() < 0.03

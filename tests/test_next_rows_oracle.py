@@ -60,3 +60,19 @@ def test_loss_weights_sum_to_one_per_unit():
         if agg == 2:  # seq-mean-token-sum: each non-empty sequence sums to its token count / seqs
             continue
         assert abs(w.sum() - 1.0) < 1e-12, agg
+
+
+def test_decode_next_matches_reference():
+    d = _load("decode.json")
+    for c in d["cases"]:
+        tok, lp = O.decode_next(np.asarray(d["rows"][c["row"]]), c["temperature"], c["seed"], c["version"],
+                                c["sample_key"], c["position"])
+        assert tok == c["ref_token"] and abs(lp - c["ref_logp"]) <= 1e-12
+        assert O.hash_str(c["sample_id"]) == c["sample_key"]
+
+
+def test_sample_key_is_reference_hash():
+    import paper_2506_06122_b200 as rlo
+    d = _load("decode.json")
+    for c in d["cases"][:20]:
+        assert rlo.sample_key(c["sample_id"]) == c["sample_key"]
