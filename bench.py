@@ -259,11 +259,10 @@ def run_ours(args, c):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, c, target_s=args.cpu_seconds)
-    if rank == 0:
-        print(json.dumps(out), flush=True)
     obj.close()
     if dist:
         dist.destroy_process_group()
+    return out if rank == 0 else None
 
 
 def _ppo(obj, rlo, cfg, tokens, lengths, logits, adv, seq_offset, logp):
@@ -413,7 +412,7 @@ def run_reference(args, c):
            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads,
                             "kind": "reference" if use_ref else "port", "sample": base["sample"]},
            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    return out
 
 
 def main():
@@ -432,10 +431,19 @@ def main():
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     c = CONFIGS[args.config]
-    if args.impl == "reference":
-        run_reference(args, c)
-    else:
-        run_ours(args, c)
+    # stdout carries exactly one JSON line: anything libraries print (NCCL's
+    # version banner, warnings) is routed to stderr while the run executes.
+    sys.stdout.flush()
+    real_stdout = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        out = run_reference(args, c) if args.impl == "reference" else run_ours(args, c)
+    finally:
+        sys.stdout.flush()
+        os.dup2(real_stdout, 1)
+        os.close(real_stdout)
+    if out is not None:
+        print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__":

@@ -147,12 +147,15 @@ std::vector<std::vector<double>> compute_advantages(rlo::Objective& obj, const r
 // ---- worker -------------------------------------------------------------------
 
 B200PolicyWorker::B200PolicyWorker(int32_t device, const rollmini::TrainConfig& train_config, LogitsProvider logits)
-    : obj_(device), train_config_(train_config), logits_(std::move(logits)) {
+    : obj_(device), train_config_(train_config), logits_(std::move(logits)), device_(device) {
   train_config_.validate();
   device_id = "cuda:" + std::to_string(device);
 }
 
 rollmini::Message B200PolicyWorker::call(const std::string& method, const rollmini::Message& input) {
+  // Cluster workers run on their own threads (cluster.cpp:171-192): bind this
+  // thread to the worker's GPU before any allocation or launch.
+  cuda_check(cudaSetDevice(device_), "B200PolicyWorker: cudaSetDevice");
   // policy_workers.cpp:46-64 dispatch for the path's methods
   if (method == "forward_logprobs") return do_forward_logprobs(input);
   if (method == "compute_gradient") return do_compute_gradient(input);

@@ -86,6 +86,7 @@ class B200PolicyWorker : public rollmini::Worker {
   rollmini::TrainConfig train_config_;
   LogitsProvider logits_;
   uint64_t version_ = 1;
+  int32_t device_ = 0;
 };
 
 // WorkerFactory (worker.hpp:47-48) for a cluster of B200 workers, one GPU each.

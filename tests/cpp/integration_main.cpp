@@ -17,6 +17,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -41,22 +43,27 @@ void check(bool ok, const std::string& what) {
 
 bool close(double g, double r, double tol = 1e-5) { return std::fabs(g - r) <= tol * std::max(1.0, std::fabs(r)); }
 
-// Device logits provider: every row of the padded view equals `row`.
+// Device logits provider: every row of the padded view equals `row`.  Called
+// from several worker threads (one per rank / GPU): one buffer per device.
 struct TiledRow {
   std::vector<float> row;
-  float* dev = nullptr;
-  size_t cap = 0;
+  std::mutex mu;
+  std::map<int, std::pair<float*, size_t>> bufs;  // device -> (buffer, capacity)
   rlo_logits operator()(const SampleBatch& batch, int32_t T) {
     const size_t V = row.size(), rows = batch.size() * static_cast<size_t>(T);
+    int dev = 0;
+    cudaGetDevice(&dev);  // the calling worker bound its GPU
+    std::lock_guard<std::mutex> lock(mu);
+    auto& [ptr, cap] = bufs[dev];
     if (rows * V > cap) {
-      if (dev) cudaFree(dev);
+      if (ptr) cudaFree(ptr);
       cap = rows * V;
-      cudaMalloc(&dev, sizeof(float) * cap);
+      cudaMalloc(&ptr, sizeof(float) * cap);
     }
     std::vector<float> host(rows * V);
     for (size_t r = 0; r < rows; ++r) std::memcpy(host.data() + r * V, row.data(), sizeof(float) * V);
-    cudaMemcpy(dev, host.data(), sizeof(float) * host.size(), cudaMemcpyHostToDevice);
-    return rlo_logits{dev, RLO_DTYPE_F32, static_cast<int32_t>(V), static_cast<int64_t>(V)};
+    cudaMemcpy(ptr, host.data(), sizeof(float) * host.size(), cudaMemcpyHostToDevice);
+    return rlo_logits{ptr, RLO_DTYPE_F32, static_cast<int32_t>(V), static_cast<int64_t>(V)};
   }
 };
 
@@ -102,7 +109,8 @@ int main() {
   cfg.kl_coef = 0.1;
   const Vocabulary& vocab = Vocabulary::standard();
   (void)vocab;
-  TiledRow tiles{std::vector<float>(row)};
+  TiledRow tiles;
+  tiles.row = row;
   auto provider = [&tiles](const SampleBatch& b, int32_t T) { return tiles(b, T); };
 
   PolicyWorker ref_worker(params, Vocabulary::standard(), cfg);
