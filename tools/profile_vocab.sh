@@ -1,4 +1,5 @@
 # ncu evidence for the default vocab kernels (one GPU; plain run first, exit 0, then ncu).
+./build/integration_test | tail -1
 C2="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
 C3="python bench.py --config 3 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
 $C2 > gpurun_out/plain2.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_cfg2_v2.csv $C2 > gpurun_out/ncu_l2.log 2>&1; echo l2=$?
