@@ -334,6 +334,52 @@ rlo_status rlo_decode_sample(rlo_handle* h, const rlo_logits* logits, int32_t n_
 /* rng::hash_str (rng.hpp:34-41): the per-sample key of a sample_id. Host only. */
 uint64_t rlo_sample_key(const char* sample_id);
 
+/* ---- wire format + parameter sync (§8f row 4) ---------------------------- */
+
+/* A SampleBatch parsed from the reference's JSONL wire format
+ * (SampleBatch::from_jsonl, sample.cpp:124-159) into padded HOST arrays
+ * (malloc'ed; free with rlo_host_batch_free).  T = longest response.  Arrays a
+ * batch does not carry at all are NULL.  mask: 1 for samples with an empty
+ * action_mask (sample.hpp:31).  rewards: per-token rewards, with a sample
+ * that has only scalar_reward getting it on its last token (policy.cpp:265-271);
+ * scalar_rewards: NaN where absent.  first_missing_reward: first sample with
+ * neither (compute_advantages' InputError, policy.cpp:274-275), else -1.
+ * sample_keys = rng::hash_str(sample_id); group_index = group_id in order of
+ * first appearance. */
+typedef struct rlo_host_batch {
+  int32_t B, T;
+  int32_t first_missing_reward;
+  int32_t reserved;
+  int32_t* lengths;
+  int32_t* tokens;
+  uint8_t* mask;
+  float* rewards;
+  float* scalar_rewards;
+  float* response_logprobs;
+  float* ref_logprobs;
+  float* advantages;
+  uint64_t* sample_keys;
+  int32_t* group_index;
+} rlo_host_batch;
+
+/* Parse + SampleBatch::validate (sample.cpp:85-102, same messages).  Host only. */
+rlo_status rlo_batch_from_jsonl(const char* text, size_t len, rlo_host_batch** out);
+void rlo_host_batch_free(rlo_host_batch* batch);
+
+/* bucket_plan (policy.cpp:542-548): contiguous bucket sizes (each <=
+ * bucket) covering total elements, ceiling division with a short tail
+ * ({0} for total 0).  out has room for *n_buckets entries on input; the count
+ * is returned in *n_buckets.  Host only. */
+rlo_status rlo_bucket_plan(uint64_t total, uint64_t bucket, uint64_t* out, int64_t* n_buckets);
+
+/* ModelUpdateGroup (sync_params policy_workers.cpp:234-260):
+ * broadcast a device buffer from `root` to every rank of the handle's NCCL
+ * group in contiguous buckets of at most bucket_bytes (NVLink; the
+ * reference's bucketed train -> infer parameter sync).  Destinations end
+ * bit-identical.  Stream-ordered. */
+rlo_status rlo_broadcast_params(rlo_handle* h, void* buffer, uint64_t bytes, uint64_t bucket_bytes, int32_t root,
+                                void* stream);
+
 /* Synchronise `stream` and report device-side input errors (OOV tokens). */
 rlo_status rlo_sync(rlo_handle* h, void* stream);
 

@@ -367,3 +367,29 @@ def ref_decode_b2(row, temperature, seed, version, sample_key, position):
 def ref_hash_str(s):
     ref().ref_hash_str.restype = C.c_uint64
     return int(ref().ref_hash_str(s.encode()))
+
+
+# ---- wire format / bucket plan ------------------------------------------------
+
+def ref_batch_jsonl(seed, n):
+    """SampleBatch::to_jsonl (sample.cpp:144-148) of a random batch (reference code)."""
+    size = ref().ref_batch_jsonl(C.c_uint64(seed), C.c_int32(n), None, C.c_int64(0))
+    ref().ref_batch_jsonl.restype = C.c_int64
+    size = ref().ref_batch_jsonl(C.c_uint64(seed), C.c_int32(n), None, C.c_int64(0))
+    buf = C.create_string_buffer(int(size) + 1)
+    ref().ref_batch_jsonl(C.c_uint64(seed), C.c_int32(n), buf, C.c_int64(size))
+    return buf.raw[:size].decode("utf-8")
+
+
+def ref_bucket_plan(total, bucket):
+    out = np.zeros(max(1, -(-total // bucket)) + 1, dtype=np.uint64)
+    n = C.c_int64()
+    ref().ref_bucket_plan(C.c_uint64(total), C.c_uint64(bucket), _p(out), C.byref(n))
+    return out[:n.value].tolist()
+
+
+def ref_parse_validate_jsonl(text):
+    """(code, message) of SampleBatch::from_jsonl(text).validate() in the reference."""
+    err = C.create_string_buffer(512)
+    code = ref().ref_parse_validate_jsonl(text.encode("utf-8"), err, C.c_int32(512))
+    return int(code), err.value.decode()

@@ -230,6 +230,48 @@ int32_t ref_decode_b2(const double* row, int32_t V, double temperature, uint64_t
 
 uint64_t ref_hash_str(const char* s) { return rng::hash_str(s); }
 
+// SampleBatch::to_jsonl (sample.cpp:144-148) of a random batch exercising every
+// field and presence pattern; returns the text length (writes up to cap bytes).
+int64_t ref_batch_jsonl(uint64_t seed, int32_t n, char* out, int64_t cap) {
+  rng::Stream s(seed);
+  SampleBatch batch;
+  for (int32_t i = 0; i < n; ++i) {
+    SampleRecord r;
+    r.sample_id = "s" + std::to_string(i) + (i % 5 == 0 ? "\"q\\u\t\xc3\xa9" : "");
+    r.group_id = "g" + std::to_string(i / 3);
+    r.domain_tag = i % 2 ? "math" : "code";
+    const size_t np = 1 + s.next_below(4), nr = s.next_below(7);
+    for (size_t t = 0; t < np; ++t) r.prompt_tokens.push_back(static_cast<int>(s.next_below(52)));
+    for (size_t t = 0; t < nr; ++t) r.response_tokens.push_back(static_cast<int>(s.next_below(52)));
+    const uint64_t pat = s.next_below(64);
+    for (size_t t = 0; t < nr; ++t) {
+      if (pat & 1) r.response_logprobs.push_back(-3.0 * s.next_double());
+      if (pat & 2) r.ref_logprobs.push_back(-3.0 * s.next_double() - 1e-7);
+      if (pat & 4) r.rewards.push_back(s.next_double() < 0.8 ? 0.0 : 2.0 * s.next_double() - 1.0);
+      if (pat & 8) r.advantages.push_back(s.next_gaussian());
+      if (pat & 16) r.action_mask.push_back(s.next_double() < 0.7 ? 1 : 0);
+    }
+    if (pat & 32) r.scalar_reward = s.next_double() * 3.0 - 1.0;
+    r.done = (pat & 1) != 0;
+    if (i % 4 == 0) r.meta["gold"] = std::to_string(i);
+    batch.push_back(std::move(r));
+  }
+  const std::string text = batch.to_jsonl();
+  if (out && cap > 0) std::memcpy(out, text.data(), std::min<size_t>(text.size(), static_cast<size_t>(cap)));
+  return static_cast<int64_t>(text.size());
+}
+
+// SampleBatch::from_jsonl + validate (sample.cpp:85-102, 150-158) on `text`.
+int32_t ref_parse_validate_jsonl(const char* text, char* err, int32_t errlen) {
+  return guarded(err, errlen, [&] { SampleBatch::from_jsonl(text).validate(); });
+}
+
+void ref_bucket_plan(uint64_t total, uint64_t bucket, uint64_t* out, int64_t* n) {
+  auto p = bucket_plan(static_cast<size_t>(total), static_cast<size_t>(bucket));
+  *n = static_cast<int64_t>(p.size());
+  for (size_t i = 0; i < p.size(); ++i) out[i] = p[i];
+}
+
 // merge_gradients (policy.cpp:421-450) on scalar partials with empty grads.
 int32_t ref_merge_scalars(const double* parts5, int32_t nranks, double* out5, char* err, int32_t errlen) {
   return guarded(err, errlen, [&] {

@@ -59,6 +59,15 @@ class rlo_value_stats(C.Structure):
                 ("tokens", C.c_uint64)]
 
 
+class rlo_host_batch(C.Structure):
+    _fields_ = [("B", C.c_int32), ("T", C.c_int32), ("first_missing_reward", C.c_int32), ("reserved", C.c_int32),
+                ("lengths", C.POINTER(C.c_int32)), ("tokens", C.POINTER(C.c_int32)), ("mask", C.POINTER(C.c_uint8)),
+                ("rewards", C.POINTER(C.c_float)), ("scalar_rewards", C.POINTER(C.c_float)),
+                ("response_logprobs", C.POINTER(C.c_float)), ("ref_logprobs", C.POINTER(C.c_float)),
+                ("advantages", C.POINTER(C.c_float)), ("sample_keys", C.POINTER(C.c_uint64)),
+                ("group_index", C.POINTER(C.c_int32))]
+
+
 class rlo_partials(C.Structure):
     _fields_ = [("v", C.c_double * NPARTIAL)]
 
@@ -116,6 +125,10 @@ def lib() -> C.CDLL:
         "rlo_value_loss": ([vp, P(rlo_batch), vp, vp, vp, C.c_double, vp, P(rlo_value_stats), vp], C.c_int),
         "rlo_decode_sample": ([vp, P(rlo_logits), i32, C.c_double, u64, u64, vp, vp, vp, vp, vp], C.c_int),
         "rlo_sample_key": ([C.c_char_p], u64),
+        "rlo_batch_from_jsonl": ([C.c_char_p, C.c_size_t, P(P(rlo_host_batch))], C.c_int),
+        "rlo_host_batch_free": ([P(rlo_host_batch)], None),
+        "rlo_bucket_plan": ([u64, u64, P(u64), P(i64)], C.c_int),
+        "rlo_broadcast_params": ([vp, vp, u64, u64, i32, vp], C.c_int),
         "rlo_synth_logits": ([vp, i32, i64, i32, i64, u64, i32, i64, vp], C.c_int),
         "rlo_synth_tokens": ([vp, i64, i32, u64, i64, i64, vp], C.c_int),
     }

@@ -30,13 +30,17 @@ std::atomic<uint64_t> g_launches{0};
 using namespace rlo;
 
 namespace {
-
 thread_local std::string g_last_error;
+}  // namespace
 
-rlo_status fail(rlo_status code, const std::string& msg) {
+rlo_status rlo::set_last_error(rlo_status code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
+
+namespace {
+
+rlo_status fail(rlo_status code, const std::string& msg) { return set_last_error(code, msg); }
 
 rlo_status cuda_fail(cudaError_t e, const char* where) {
   return fail(RLO_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -57,10 +61,11 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   std::string error;
-  bool ok() const { return GetUniqueId && CommInitRank && AllGather && CommDestroy && GetErrorString; }
+  bool ok() const { return GetUniqueId && CommInitRank && AllGather && Broadcast && CommDestroy && GetErrorString; }
 };
 
 const NcclApi& nccl_api() {
@@ -78,6 +83,7 @@ const NcclApi& nccl_api() {
     a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
     a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
     a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+    a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(dlsym(h, "ncclBroadcast"));
     a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
     if (!a.ok()) a.error = "libnccl.so.2 lacks a required symbol";
@@ -811,6 +817,40 @@ rlo_status rlo_decode_sample(rlo_handle* h, const rlo_logits* logits, int32_t n_
   DeviceGuard g(h->device);
   RLO_CUDA(launch_decode(logits->data, logits->dtype, logits->row_stride, logits->V, n_rows, temperature, seed, version,
                          sample_keys, positions, out_tokens, out_logp, h->num_sms, static_cast<cudaStream_t>(stream)));
+  return RLO_OK;
+}
+
+rlo_status rlo_bucket_plan(uint64_t total, uint64_t bucket, uint64_t* out, int64_t* n_buckets) {
+  // bucket_plan, policy.cpp:542-548
+  if (bucket == 0) return fail(RLO_ERR_CONFIG, "bucket_plan: bucket_size must be positive");
+  if (!n_buckets) return fail(RLO_ERR_INPUT, "bucket_plan: null count");
+  const int64_t need = total == 0 ? 1 : static_cast<int64_t>((total + bucket - 1) / bucket);
+  const int64_t room = *n_buckets;
+  *n_buckets = need;
+  if (!out || room < need) return fail(RLO_ERR_INPUT, "bucket_plan: output has room for fewer buckets than needed");
+  if (total == 0) {
+    out[0] = 0;
+    return RLO_OK;
+  }
+  int64_t i = 0;
+  for (uint64_t off = 0; off < total; off += bucket) out[i++] = std::min(bucket, total - off);
+  return RLO_OK;
+}
+
+rlo_status rlo_broadcast_params(rlo_handle* h, void* buffer, uint64_t bytes, uint64_t bucket_bytes, int32_t root,
+                                void* stream) {
+  if (!h) return fail(RLO_ERR_INPUT, "broadcast_params: null handle");
+  if (bucket_bytes == 0) return fail(RLO_ERR_CONFIG, "sync_params: bucket_size must be positive");  // policy_workers.cpp:235
+  if (root < 0 || root >= (h->comm ? h->world : 1)) return fail(RLO_ERR_CONFIG, "broadcast_params: root out of range");
+  if (!h->comm || bytes == 0) return RLO_OK;  // a group of one already holds the parameters
+  if (!buffer) return fail(RLO_ERR_INPUT, "broadcast_params: null buffer");
+  DeviceGuard g(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* p = static_cast<char*>(buffer);
+  for (uint64_t off = 0; off < bytes; off += bucket_bytes) {  // contiguous buckets, bucket_plan order
+    const uint64_t n = std::min(bucket_bytes, bytes - off);
+    RLO_NCCL(nccl_api().Broadcast(p + off, p + off, n, ncclUint8, root, h->comm, s));
+  }
   return RLO_OK;
 }
 

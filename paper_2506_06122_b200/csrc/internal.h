@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <string>
 #include <cmath>
 
 #include "../../include/rlo.h"
@@ -13,6 +14,9 @@
 namespace rlo {
 
 extern std::atomic<uint64_t> g_launches;
+
+// Records the calling thread's rlo_last_error() message and returns `code`.
+rlo_status set_last_error(rlo_status code, const std::string& msg);
 
 // Roles of the (up to 3) logits tensors a vocab pass reads.
 enum Role : int32_t { ROLE_ACTOR = 0, ROLE_OLD = 1, ROLE_REF = 2 };

@@ -2,9 +2,10 @@
 //
 // The reference accumulates GradAccum scalars in token order and merges
 // ranks in rank order (policy.cpp:366-370, :428-436; SPEC.md:278 fixed
-// reduction order).  Here: per-token results (vocab.cu) -> one warp per
-// sequence sums its tokens in fp64 (lane-strided + butterfly: a fixed order)
-// -> one CTA reduces the sequence records into the rank's partials, including
+// reduction order).  Here: per-token results (vocab.cu) -> one CTA per
+// sequence sums its tokens in fp64 (thread-strided, butterfly, warps in
+// order: a fixed order) -> one CTA reduces the sequence records into the
+// rank's partials, including
 // the sequence- and group-level aggregation sums.  No floating-point atomics
 // anywhere, so results are bitwise reproducible run to run.
 #include "common.cuh"
@@ -13,42 +14,49 @@
 namespace rlo {
 namespace {
 
-constexpr int kSeqWarps = 8;
+constexpr int kSeqThreads = 256;  // one CTA per sequence: long responses (T up to 16384) stay parallel
 
-__global__ void __launch_bounds__(kSeqWarps * 32)
+__global__ void __launch_bounds__(kSeqThreads)
     seq_reduce_kernel(int B, int T, int seq_offset, const int32_t* __restrict__ lengths,
                       const uint8_t* __restrict__ mask, const float* __restrict__ s_loss,
                       const float* __restrict__ s_ratio, const float* __restrict__ s_kl,
                       const float* __restrict__ s_ent, const uint8_t* __restrict__ s_flags, SeqRec* recs) {
+  __shared__ double sm[9][kSeqThreads / 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.x * kSeqWarps + warp;
-  if (b >= B) return;
+  const int b = blockIdx.x;
   const int n = seq_len(lengths, b, T);
-  double loss = 0, ratio = 0, kl = 0, ent = 0, clipped = 0, dual = 0, tokens = 0, nfg = 0, nfl = 0;
-  for (int t = lane; t < n; t += 32) {
+  double v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // loss ratio kl ent | clipped dual tokens nfg nfl
+  int c[5] = {0, 0, 0, 0, 0};
+  for (int t = threadIdx.x; t < n; t += kSeqThreads) {
     const int64_t i = (int64_t)b * T + t;
     if (mask && !mask[i]) continue;
     const uint8_t f = s_flags[i];
-    loss += (double)s_loss[i];
-    ratio += (double)s_ratio[i];
-    kl += (double)s_kl[i];
-    ent += (double)s_ent[i];
-    clipped += (f & TF_CLIPPED) ? 1.0 : 0.0;
-    dual += (f & TF_DUAL) ? 1.0 : 0.0;
-    nfg += (f & TF_NONFINITE_GRAD) ? 1.0 : 0.0;
-    nfl += (f & TF_NONFINITE_LOSS) ? 1.0 : 0.0;
-    tokens += 1.0;
+    v[0] += (double)s_loss[i];
+    v[1] += (double)s_ratio[i];
+    v[2] += (double)s_kl[i];
+    v[3] += (double)s_ent[i];
+    c[0] += (f & TF_CLIPPED) ? 1 : 0;
+    c[1] += (f & TF_DUAL) ? 1 : 0;
+    c[2] += 1;
+    c[3] += (f & TF_NONFINITE_GRAD) ? 1 : 0;
+    c[4] += (f & TF_NONFINITE_LOSS) ? 1 : 0;
   }
-  loss = warp_sum(loss);
-  ratio = warp_sum(ratio);
-  kl = warp_sum(kl);
-  ent = warp_sum(ent);
-  clipped = warp_sum(clipped);
-  dual = warp_sum(dual);
-  tokens = warp_sum(tokens);
-  nfg = warp_sum(nfg);
-  nfl = warp_sum(nfl);
-  if (lane == 0) recs[seq_offset + b] = SeqRec{loss, ratio, kl, ent, clipped, dual, tokens, nfg, nfl, 0.0};
+#pragma unroll
+  for (int k = 0; k < 5; ++k) v[4 + k] = (double)c[k];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {  // fixed shuffle tree, then warps in order: deterministic
+    v[k] = warp_sum(v[k]);
+    if (lane == 0) sm[k][warp] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r[9];
+    for (int k = 0; k < 9; ++k) {
+      r[k] = 0.0;
+      for (int w = 0; w < kSeqThreads / 32; ++w) r[k] += sm[k][w];
+    }
+    recs[seq_offset + b] = SeqRec{r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7], r[8], 0.0};
+  }
 }
 
 constexpr int kBR = 1024;
@@ -114,7 +122,7 @@ cudaError_t launch_seq_reduce(int32_t B, int32_t T, int32_t seq_offset, const in
                               const float* s_kl, const float* s_ent, const uint8_t* s_flags, SeqRec* recs,
                               cudaStream_t s) {
   if (B == 0) return cudaSuccess;
-  seq_reduce_kernel<<<(B + kSeqWarps - 1) / kSeqWarps, kSeqWarps * 32, 0, s>>>(
+  seq_reduce_kernel<<<B, kSeqThreads, 0, s>>>(
       B, T, seq_offset, lengths, mask, s_loss, s_ratio, s_kl, s_ent, s_flags, recs);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();

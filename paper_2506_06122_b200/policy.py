@@ -337,6 +337,13 @@ class Objective:
                                         C.byref(st), _stream(stream, self.device)))
         return {k: getattr(st, k) for k, _ in st._fields_}, dv
 
+    def broadcast_params(self, buffer, bucket_bytes: int, root: int = 0, stream=None) -> None:
+        """ModelUpdateGroup: bucketed NCCL broadcast of a device tensor from `root`
+        (sync_params, policy_workers.cpp:234-260)."""
+        check(_abi.lib().rlo_broadcast_params(self._h, C.c_void_p(buffer.data_ptr()),
+                                              buffer.numel() * buffer.element_size(), bucket_bytes, root,
+                                              _stream(stream, self.device)))
+
     def decode_sample(self, logits, temperature, seed, version, sample_keys, positions, stream=None):
         """decode_next (policy.cpp:143-169) per row: (tokens int32, untempered logp float32)."""
         torch = _torch()
@@ -456,3 +463,39 @@ class PolicyWorker:
 def sample_key(sample_id: str) -> int:
     """rng::hash_str (rng.hpp:34-41): the per-sample key decode_next draws with."""
     return int(_abi.lib().rlo_sample_key(sample_id.encode()))
+
+
+def batch_from_jsonl(text) -> dict:
+    """SampleBatch::from_jsonl (sample.cpp:150-158) + validate, into padded numpy arrays
+    (keys of rlo_host_batch; absent arrays are None)."""
+    data = text.encode("utf-8") if isinstance(text, str) else bytes(text)
+    hb = C.POINTER(_abi.rlo_host_batch)()
+    check(_abi.lib().rlo_batch_from_jsonl(data, len(data), C.byref(hb)))
+    try:
+        b = hb.contents
+        B, T = b.B, b.T
+        out = {"B": B, "T": T, "first_missing_reward": b.first_missing_reward}
+
+        def arr(ptr, n, shape):
+            return None if not ptr else np.ctypeslib.as_array(ptr, shape=(n,)).copy().reshape(shape)
+
+        out["lengths"] = arr(b.lengths, B, (B,))
+        out["tokens"] = arr(b.tokens, B * T, (B, T))
+        out["mask"] = arr(b.mask, B * T, (B, T))
+        for k in ("rewards", "response_logprobs", "ref_logprobs", "advantages"):
+            out[k] = arr(getattr(b, k), B * T, (B, T))
+        out["scalar_rewards"] = arr(b.scalar_rewards, B, (B,))
+        out["sample_keys"] = arr(b.sample_keys, B, (B,))
+        out["group_index"] = arr(b.group_index, B, (B,))
+        return out
+    finally:
+        _abi.lib().rlo_host_batch_free(hb)
+
+
+def bucket_plan(total: int, bucket: int) -> list[int]:
+    """bucket_plan (policy.cpp:542-548)."""
+    n = C.c_int64(0)
+    _abi.lib().rlo_bucket_plan(total, bucket, None, C.byref(n))  # sizing call
+    out = (C.c_uint64 * max(1, n.value))()
+    check(_abi.lib().rlo_bucket_plan(total, bucket, out, C.byref(n)))
+    return list(out[:n.value])

@@ -200,6 +200,21 @@ def decode_cases(rng):
                    "cases": cases}, f)
 
 
+def jsonl_cases():
+    """SampleBatch::to_jsonl (sample.cpp:144-148): the reference's own wire text."""
+    with open(os.path.join(HERE, "batch.jsonl"), "w", encoding="utf-8") as f:
+        f.write(O.ref_batch_jsonl(2506, 40))
+    bad = {
+        "duplicate_id": '{"sample_id":"a","response_tokens":[1]}\n{"sample_id":"a","response_tokens":[2]}\n',
+        "length_mismatch": '{"sample_id":"x","response_tokens":[1,2,3],"rewards":[0.0,1.0]}\n',
+        "mask_mismatch": '{"sample_id":"y","response_tokens":[1,2],"action_mask":[1]}\n',
+    }
+    jsonl_errors = {k: list(O.ref_parse_validate_jsonl(v)) + [v] for k, v in bad.items()}
+    plans = [dict(total=t, bucket=b, plan=O.ref_bucket_plan(t, b))
+             for t, b in [(1000, 256), (0, 7), (7, 7), (8, 7), (207, 1), (1 << 20, 65536), (1000003, 4096)]]
+    return {"bucket_plan": plans, "jsonl_errors": jsonl_errors}
+
+
 def config_cases():
     """TrainConfig::validate messages (policy.cpp:29-37) and split_sizes (sample.cpp:99-105)."""
     bad = [dict(clip_eps=0.0), dict(clip_eps=1.0), dict(kl_coef=-0.1), dict(learning_rate=-1.0),
@@ -223,6 +238,7 @@ def main():
     ppo_cases(rng)
     value_cases(np.random.default_rng(474))
     decode_cases(np.random.default_rng(143))
+    extra.update(jsonl_cases())
     cfgs, splits = config_cases()
     with open(os.path.join(HERE, "misc.json"), "w") as f:
         json.dump({"train_config_validate": cfgs, "split_sizes": splits, **extra}, f, indent=1)

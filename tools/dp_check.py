@@ -88,6 +88,21 @@ def main():
                   f"adv max err {a_err:.2e}, tokens {st.tokens}", flush=True)
             fails += not ok
             single.close()
+    # ModelUpdateGroup: bucketed broadcast, destinations bit-identical for every
+    # bucket size (test_policy_workers.cpp:100-130's sync_params property)
+    n_params = 1_000_003
+    for bucket in (4, 28, 4096, 1 << 20, 4 * n_params):
+        gen = torch.Generator(device=dev).manual_seed(1234)
+        src = torch.randn(n_params, device=dev, generator=gen)
+        buf = src.clone() if rank == 0 else torch.zeros_like(src)
+        obj.broadcast_params(buf, bucket_bytes=bucket, root=0)
+        ok = bool(torch.equal(buf, src))  # every rank can regenerate rank 0's values
+        okt = torch.tensor([int(ok)], device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            good = bool(okt.item())
+            print(f"{'PASS' if good else 'FAIL'} dp{world} broadcast_params bucket={bucket} bytes: bit-identical", flush=True)
+            fails += not good
     obj.close()
     flag = torch.tensor([fails], device=dev)
     dist.broadcast(flag, src=0)
