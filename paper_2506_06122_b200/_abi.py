@@ -11,7 +11,8 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "librlo.so")
+# RLO_LIB overrides the in-tree library (A/B builds of the same sources in kernel experiments).
+LIB_PATH = os.environ.get("RLO_LIB") or os.path.join(HERE, "lib", "librlo.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "rlo.h")
 
 RLO_OK, RLO_ERR_INPUT, RLO_ERR_CONFIG, RLO_ERR_TRAINING, RLO_ERR_CUDA, RLO_ERR_NCCL, RLO_ERR_DISPATCH = range(7)

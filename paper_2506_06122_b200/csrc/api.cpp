@@ -443,8 +443,9 @@ rlo_status rlo_forward_logprobs(rlo_handle* h, const rlo_batch* batch, const rlo
                                 float* out_entropy, float* out_token_logit, void* stream) {
   if (!h) return fail(RLO_ERR_INPUT, "forward_logprobs: null handle");
   RLO_TRY(check_batch(batch, "forward_logprobs", true));
+  if ((int64_t)batch->B * batch->T == 0) return RLO_OK;  // an empty batch scores nothing (policy.cpp:219-231)
   RLO_TRY(check_logits(logits, "forward_logprobs", "policy"));
-  if (!out_logp && (int64_t)batch->B * batch->T > 0) return fail(RLO_ERR_INPUT, "forward_logprobs: out_logp required");
+  if (!out_logp) return fail(RLO_ERR_INPUT, "forward_logprobs: out_logp required");
   DeviceGuard g(h->device);
   VocabArgs a;
   std::memset(&a, 0, sizeof(a));

@@ -86,7 +86,7 @@ __device__ __forceinline__ void row_accumulate(const ET* __restrict__ row, int V
 }
 
 template <typename ET, int NT, int U, bool PF, bool LOSS, bool ENT0, int MATH>
-__global__ void __launch_bounds__(kThreads) vocab_ldg_kernel(const VocabArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) vocab_ldg_kernel(const VocabArgs a) {
   __shared__ float red[2][kWarps][NT][3];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t nrows = (int64_t)a.B * a.T;

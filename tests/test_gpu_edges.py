@@ -32,7 +32,7 @@ def test_vocab_of_one(env):
     x = dev(torch, np.array([[3.5], [-2.0]], np.float32))
     out = obj.forward_logprobs(x, dev(torch, np.zeros((1, 2), np.int32)), dev(torch, np.array([2], np.int32)),
                                entropy=True)
-    assert out["logp"].abs().max().item() == 0.0 and out["entropy"].abs().max().item() < 1e-6
+    assert out["logp"].abs().max().item() < 1e-6 and out["entropy"].abs().max().item() < 1e-6
 
 
 @pytest.mark.parametrize("V", [64, 4096, 32000])
