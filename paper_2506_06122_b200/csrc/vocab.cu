@@ -110,9 +110,15 @@ __global__ void __launch_bounds__(kThreads, 4) vocab_ldg_kernel(const VocabArgs 
     for (int k = 0; k < NT; ++k) {
       acc_init(acc[k]);
       const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + row * a.stride[k];
-      if (k == 0 && ENT0)
+      if (k == 0 && ENT0) {
         row_accumulate<ET, U, PF, true, MATH>(rp, a.V, vec_ok, acc[k]);
-      else
+        if (MATH != 0 && !(isfinite(acc[k].s) && isfinite(acc[k].w))) {
+          // -inf logits in this thread's share: redo it with the entropy guard
+          // (the row was just streamed, so the re-read hits L2)
+          acc_init(acc[k]);
+          row_accumulate<ET, U, PF, true, MATH | kMathGuard>(rp, a.V, vec_ok, acc[k]);
+        }
+      } else
         row_accumulate<ET, U, PF, false, MATH>(rp, a.V, vec_ok, acc[k]);
     }
 #pragma unroll

@@ -91,15 +91,20 @@ __device__ __forceinline__ void acc_warp_reduce(Acc& a) {
 __host__ __device__ constexpr int poly_deg(int math) { return math == 2 || math == 3 ? 5 : math == 4 || math == 5 ? 4 : 0; }
 __host__ __device__ constexpr bool poly_half(int math) { return math == 3 || math == 5; }
 __host__ __device__ constexpr int poly_deg_ent(int math) { return math == 4 ? 4 : 0; }
+// Template MATH values may carry kMathGuard (the guarded entropy-row variant).
+constexpr int kMathMask = 0xff;
+constexpr int kMathGuard = 0x100;
 
-template <bool ENT>
+// GUARD (entropy row only): clamp t so that -inf logits give
+// e*t = 2^-126 * -126 (negligible) instead of 0 * -inf = NaN.  The fast path
+// runs unguarded and a thread whose entropy sum comes out non-finite redoes
+// its share of the row guarded (vocab.cu), so finite rows pay nothing.
+template <bool ENT, bool GUARD>
 __device__ __forceinline__ void pair2(float zl, float zh, f2 L2, f2 nmL, f2& s, f2& w, int poly) {
   const f2 t = ffma2(pk2(zl, zh), L2, nmL);
   float tl, th;
   upk2(t, tl, th);
-  if (ENT || poly) {
-    // clamp to the normal range: the polynomial's domain, and on the entropy
-    // row -inf logits give e*t = 2^-126 * -126 (negligible) instead of 0 * -inf
+  if ((ENT && GUARD) || poly) {  // poly: clamp to the polynomial's normal-range domain
     tl = fmaxf(tl, -126.0f);
     th = fmaxf(th, -126.0f);
   }
@@ -130,8 +135,10 @@ struct Vec<float> {
     for (int u = 1; u < U; ++u) m = fmaxf(m, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
     return m;
   }
-  template <int U, bool ENT, int MATH>
+  template <int U, bool ENT, int MATHG>
   __device__ static void accumulate(const V (&v)[U], Acc& a) {
+    constexpr int MATH = MATHG & kMathMask;
+    constexpr bool G = (MATHG & kMathGuard) != 0;
     acc_rescale<ENT>(a, chunk_max<U>(v) * kL2E);
     if (MATH == 0) {
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, w0 = 0.f, w1 = 0.f, w2 = 0.f, w3 = 0.f;
@@ -149,8 +156,8 @@ struct Vec<float> {
       f2 s0 = 0, s1 = 0, w0 = 0, w1 = 0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        pair2<ENT>(v[u].x, v[u].y, L2, nmL, s0, w0, 0);
-        pair2<ENT>(v[u].z, v[u].w, L2, nmL, s1, w1, (!ENT && (u & 1)) ? poly_deg(MATH) : 0);
+        pair2<ENT, G>(v[u].x, v[u].y, L2, nmL, s0, w0, 0);
+        pair2<ENT, G>(v[u].z, v[u].w, L2, nmL, s1, w1, (!ENT && (u & 1)) ? poly_deg(MATH) : 0);
       }
       a.s += hsum2(s0, s1);
       if (ENT) a.w += hsum2(w0, w1);
@@ -178,8 +185,10 @@ struct Vec<__nv_bfloat16> {
     acc_elem<ENT>(bf16lo(x), mL, s0, w0);
     acc_elem<ENT>(bf16hi(x), mL, s1, w1);
   }
-  template <int U, bool ENT, int MATH>
+  template <int U, bool ENT, int MATHG>
   __device__ static void accumulate(const V (&v)[U], Acc& a) {
+    constexpr int MATH = MATHG & kMathMask;
+    constexpr bool G = (MATHG & kMathGuard) != 0;
     acc_rescale<ENT>(a, chunk_max<U>(v) * kL2E);
     if (MATH == 0) {
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, w0 = 0.f, w1 = 0.f, w2 = 0.f, w3 = 0.f;
@@ -197,10 +206,10 @@ struct Vec<__nv_bfloat16> {
       f2 s0 = 0, s1 = 0, w0 = 0, w1 = 0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        pair2<ENT>(bf16lo(v[u].x), bf16hi(v[u].x), L2, nmL, s0, w0, 0);
-        pair2<ENT>(bf16lo(v[u].y), bf16hi(v[u].y), L2, nmL, s1, w1, ENT ? poly_deg_ent(MATH) : poly_deg(MATH));
-        pair2<ENT>(bf16lo(v[u].z), bf16hi(v[u].z), L2, nmL, s0, w0, 0);
-        pair2<ENT>(bf16lo(v[u].w), bf16hi(v[u].w), L2, nmL, s1, w1, (ENT || !poly_half(MATH)) ? 0 : poly_deg(MATH));
+        pair2<ENT, G>(bf16lo(v[u].x), bf16hi(v[u].x), L2, nmL, s0, w0, 0);
+        pair2<ENT, G>(bf16lo(v[u].y), bf16hi(v[u].y), L2, nmL, s1, w1, ENT ? poly_deg_ent(MATH) : poly_deg(MATH));
+        pair2<ENT, G>(bf16lo(v[u].z), bf16hi(v[u].z), L2, nmL, s0, w0, 0);
+        pair2<ENT, G>(bf16lo(v[u].w), bf16hi(v[u].w), L2, nmL, s1, w1, (ENT || !poly_half(MATH)) ? 0 : poly_deg(MATH));
       }
       a.s += hsum2(s0, s1);
       if (ENT) a.w += hsum2(w0, w1);

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kThreadsTma, 1) vocab_tma_kernel(const VocabAr
           phase ^= 1u;
         }
         if (k == 0 && ENT0)
-          VT::template accumulate<kPer, true, MATH>(v, acc[k]);
+          VT::template accumulate<kPer, true, MATH | kMathGuard>(v, acc[k]);  // streamed: no redo, always guarded
         else
           VT::template accumulate<kPer, false, MATH>(v, acc[k]);
       }
