@@ -77,7 +77,7 @@ __device__ __forceinline__ void row_accumulate(const ET* __restrict__ row, int V
   // scalar tail (or the whole row when rows are not 16-byte aligned)
   for (int i = nvec * VT::kElems + tid; i < V; i += kThreads) {
     const float z = VT::scalar(row + i);
-    acc_rescale<ENT>(a, z * kL2E);
+    acc_rescale<ENT>(a, z);
     float w = 0.f, s = 0.f;
     acc_elem<ENT>(z, a.mL, s, w);
     a.s += s;

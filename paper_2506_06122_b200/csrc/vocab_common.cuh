@@ -31,8 +31,13 @@ __device__ __forceinline__ void acc_init(Acc& a) {
   a.w = 0.f;
 }
 
+// zmax = the chunk's largest logit.  newmL is rounded explicitly (__fmul_rn):
+// a contracted d = fma(-zmax, kL2E, mL) would rescale s by the unrounded max
+// while the elements use the rounded one, an lse error of up to ulp(mL)/2 --
+// 2e-4 nats at |z| ~ 1e4.
 template <bool ENT>
-__device__ __forceinline__ void acc_rescale(Acc& a, float newmL) {
+__device__ __forceinline__ void acc_rescale(Acc& a, float zmax) {
+  const float newmL = __fmul_rn(zmax, kL2E);
   if (newmL > a.mL) {
     const float d = a.mL - newmL;
     const float sc = ex2(d);
@@ -139,7 +144,7 @@ struct Vec<float> {
   __device__ static void accumulate(const V (&v)[U], Acc& a) {
     constexpr int MATH = MATHG & kMathMask;
     constexpr bool G = (MATHG & kMathGuard) != 0;
-    acc_rescale<ENT>(a, chunk_max<U>(v) * kL2E);
+    acc_rescale<ENT>(a, chunk_max<U>(v));
     if (MATH == 0) {
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, w0 = 0.f, w1 = 0.f, w2 = 0.f, w3 = 0.f;
 #pragma unroll
@@ -189,7 +194,7 @@ struct Vec<__nv_bfloat16> {
   __device__ static void accumulate(const V (&v)[U], Acc& a) {
     constexpr int MATH = MATHG & kMathMask;
     constexpr bool G = (MATHG & kMathGuard) != 0;
-    acc_rescale<ENT>(a, chunk_max<U>(v) * kL2E);
+    acc_rescale<ENT>(a, chunk_max<U>(v));
     if (MATH == 0) {
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, w0 = 0.f, w1 = 0.f, w2 = 0.f, w3 = 0.f;
 #pragma unroll
