@@ -225,6 +225,10 @@ def run_ours(args, c):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
 
+    # ---- P=1: actor-only pass, old/ref log-probs precomputed ----
+    p1 = None if args.no_p1 else run_p1(args, c, obj, rlo, torch, cfg, logits, tokens, dside, adv, logp, stream,
+                                       barrier, dist, mb, esz)
+
     # ---- e2e: the reference-facing host-buffer call ------------------------
     e2e = None if args.no_e2e else run_e2e(args, c, obj, rlo, torch, cfg, logits, side, dev, stream, dist,
                                            key_rows, mb)
@@ -252,6 +256,7 @@ def run_ours(args, c):
                      "kernel": "vocab_kernel (fused 3-tensor logprob+entropy+loss pass, incl. per-seq reduce)",
                      "bytes_per_launch": bytes_per_launch, "avg_launch_ms": vocab_avg_ms},
         "e2e": e2e,
+        "p1": p1,
         "gpu_launches": launches,
         "clocks": clk.result(),
         "stats": {"loss": st.loss, "mean_ratio": st.mean_ratio, "clip_fraction": st.clip_fraction,
@@ -265,7 +270,9 @@ def run_ours(args, c):
     return out if rank == 0 else None
 
 
-def _ppo(obj, rlo, cfg, tokens, lengths, logits, adv, seq_offset, logp):
+def _ppo(obj, rlo, cfg, tokens, lengths, logits, adv, seq_offset, logp, old_lp=None, ref_lp=None):
+    """One fused vocab pass: logits = [actor, old, ref] (P=3) or [actor] with
+    precomputed old/ref log-probs (P=1)."""
     import ctypes as C
 
     from paper_2506_06122_b200 import _abi
@@ -274,10 +281,66 @@ def _ppo(obj, rlo, cfg, tokens, lengths, logits, adv, seq_offset, logp):
     o = _abi.rlo_token_out()
     o.logp = logp.data_ptr()
     L = [_logits(x) for x in logits]
+    vp = lambda t: None if t is None else C.c_void_p(t.data_ptr())  # noqa: E731
     check(_abi.lib().rlo_ppo_gradient(obj._h, C.byref(cfg.to_c()), C.byref(_batch(lengths, tokens, None,
                                                                                     tokens.shape[1], seq_offset)),
-                                      C.byref(L[0]), C.byref(L[1]), C.byref(L[2]), None, None,
+                                      C.byref(L[0]), C.byref(L[1]) if len(L) > 1 else None,
+                                      C.byref(L[2]) if len(L) > 2 else None, vp(old_lp), vp(ref_lp),
                                       C.c_void_p(adv.data_ptr()), C.byref(o), _stream(None, logp.device)))
+
+
+def run_p1(args, c, obj, rlo, torch, cfg, logits, tokens, dside, adv, logp, stream, barrier, dist, mb, esz):
+    """The reference pipeline's shape: old log-probs come from sampling time
+    (policy.cpp:356) and ref log-probs from a separate pass (pipeline.cpp:508),
+    so the update reads only the actor logits (P=1).  old/ref log-probs are
+    computed once here (untimed) with forward_logprobs."""
+    B, T, V = c["B"], c["T"], c["V"]
+    old_lp = torch.empty(B, T, dtype=torch.float32, device=tokens.device)
+    ref_lp = torch.empty_like(old_lp)
+    for i in range(B // mb):
+        s = slice(i * mb, (i + 1) * mb)
+        old_lp[s] = obj.forward_logprobs(logits[1], tokens[s], dside["lengths"][s])["logp"]
+        ref_lp[s] = obj.forward_logprobs(logits[2], tokens[s], dside["lengths"][s])["logp"]
+    ev = []
+
+    def step(rec):
+        obj.compute_advantages(cfg, dside["lengths"], T=T, rewards=dside.get("rewards"),
+                               scalar_rewards=dside.get("scalar_rewards"), values=dside.get("values"), out=adv)
+        for i in range(B // mb):
+            s = slice(i * mb, (i + 1) * mb)
+            if rec:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            _ppo(obj, rlo, cfg, tokens[s], dside["lengths"][s], logits[:1], adv[s], i * mb, logp[s],
+                 old_lp[s], ref_lp[s])
+            if rec:
+                e1.record(stream)
+                ev.append((e0, e1))
+        return obj.merge_gradients(cfg)
+
+    for _ in range(args.warmup):
+        step(False)
+    steps = args.steps
+    barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        st = step(True)
+    t1.record(stream)
+    barrier()
+    ms = t0.elapsed_time(t1)
+    if dist:
+        tt = torch.tensor([ms], device=tokens.device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    world = dist.get_world_size() if dist else 1
+    vk = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    bytes_per_launch = mb * T * (V * esz + 4 + 4 + 8 + 17)
+    peak, _ = load_peaks()
+    return {"value": world * B * T * steps / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms / steps,
+            "logits_tensors": 1, "achieved_gbs": bytes_per_launch / (vk * 1e-3) / 1e9,
+            "frac": bytes_per_launch / (vk * 1e-3) / 1e9 / peak, "avg_launch_ms": vk,
+            "loss": st.loss, "note": "actor logits only; old/ref log-probs precomputed (untimed)"}
 
 
 def run_e2e(args, c, obj, rlo, torch, cfg, logits, side, dev, stream, dist, key_rows, mb):
@@ -425,6 +488,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
+    ap.add_argument("--no-p1", action="store_true", help="skip the actor-only (P=1) leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-step-seconds", type=float, default=4.0)
     args = ap.parse_args()

@@ -299,6 +299,16 @@ rlo_status rlo_objective_step_host(rlo_handle* h, const rlo_train_config* cfg, i
 rlo_status rlo_loss_weights(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch,
                             const rlo_stats* stats, float* out_w, void* stream);
 
+/* The aggregation normalisers of a batch BEFORE its vocab pass: loss-
+ * participating tokens, sequences with at least one such token and groups
+ * (cfg.group_size consecutive samples) with at least one, summed over the
+ * communicator's ranks in rank order (the counts merge_gradients derives,
+ * policy.cpp:437-440).  Fills out->tokens / seqs / groups, zeroes the rest, so
+ * `out` can feed rlo_loss_weights ahead of rlo_ppo_gradient_fused.
+ * Synchronises `stream`. */
+rlo_status rlo_batch_counts(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch, rlo_stats* out,
+                            void* stream);
+
 /* Actor backward epilogue (policy.cpp:375-379): for every row with
  * weight*dlogp != 0, grad[v] = weight*dlogp*(1[v == token] - exp(z_v - lse)),
  * recomputing the softmax from the row and its lse (never stored); all
@@ -308,6 +318,22 @@ rlo_status rlo_loss_weights(rlo_handle* h, const rlo_train_config* cfg, const rl
 rlo_status rlo_logits_backward(rlo_handle* h, const rlo_batch* batch, const rlo_logits* logits, const float* lse,
                                const float* dlogp, const float* weight, void* grad, int32_t grad_dtype,
                                int64_t grad_row_stride, void* stream);
+
+/* Fused update pass: rlo_ppo_gradient (same inputs, outputs, accumulation and
+ * errors) and the actor backward epilogue in ONE read of the actor logits
+ * (policy.cpp:355-379).  A thread-block cluster holds each actor row in shared
+ * memory while the row's log-sum-exp, entropy, KL and surrogate are formed,
+ * then writes grad[v] = weight*dlogp*(1[v == token] - softmax_v) from it;
+ * rows without loss participation get zeros.  weight [B*T] must be known
+ * before the pass (rlo_batch_counts -> rlo_loss_weights).  HBM traffic per
+ * participating row P*V*s + V*s_grad instead of (P+1)*V*s + V*s_grad.  Rows
+ * that are not 16-byte aligned (or a vocabulary beyond 8 CTAs' shared memory)
+ * take the two-pass form transparently. */
+rlo_status rlo_ppo_gradient_fused(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch,
+                                  const rlo_logits* actor, const rlo_logits* old_logits, const rlo_logits* ref_logits,
+                                  const float* old_logp, const float* ref_logp, const float* advantages,
+                                  const float* weight, void* grad, int32_t grad_dtype, int64_t grad_row_stride,
+                                  const rlo_token_out* out, void* stream);
 
 /* Critic value loss (value_gradient, policy.cpp:474-540): per
  * loss-participating token err = v - return, loss 0.5*err^2, d/dv = err.

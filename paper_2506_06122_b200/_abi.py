@@ -123,6 +123,9 @@ def lib() -> C.CDLL:
         "rlo_sync": ([vp, vp], C.c_int),
         "rlo_loss_weights": ([vp, P(rlo_train_config), P(rlo_batch), P(rlo_stats), vp, vp], C.c_int),
         "rlo_logits_backward": ([vp, P(rlo_batch), P(rlo_logits), vp, vp, vp, vp, i32, i64, vp], C.c_int),
+        "rlo_batch_counts": ([vp, P(rlo_train_config), P(rlo_batch), P(rlo_stats), vp], C.c_int),
+        "rlo_ppo_gradient_fused": ([vp, P(rlo_train_config), P(rlo_batch), P(rlo_logits), P(rlo_logits),
+                                    P(rlo_logits), vp, vp, vp, vp, vp, i32, i64, P(rlo_token_out), vp], C.c_int),
         "rlo_value_loss": ([vp, P(rlo_batch), vp, vp, vp, C.c_double, vp, P(rlo_value_stats), vp], C.c_int),
         "rlo_decode_sample": ([vp, P(rlo_logits), i32, C.c_double, u64, u64, vp, vp, vp, vp, vp], C.c_int),
         "rlo_sample_key": ([C.c_char_p], u64),

@@ -106,6 +106,11 @@ const NcclApi& nccl_api() {
     if (s_ != RLO_OK) return s_;         \
   } while (0)
 
+bool getenv_flag(const char* name) {
+  const char* e = std::getenv(name);
+  return e && *e && *e != '0';
+}
+
 struct DeviceGuard {
   int prev = -1, dev;
   explicit DeviceGuard(int d) : dev(d) {
@@ -154,6 +159,7 @@ struct rlo_handle {
   int32_t acc_nseq = 0;
   // per-token scratch of the loss pass
   DevBuf<float> s_loss, s_ratio, s_kl, s_ent;
+  DevBuf<float> s_lse, s_dlogp;  // two-pass fallback of the fused update pass
   DevBuf<uint8_t> s_flags;
   // whitening
   DevBuf<WStat> wstat;
@@ -526,16 +532,25 @@ rlo_status rlo_compute_advantages(rlo_handle* h, const rlo_train_config* cfg, co
   return RLO_OK;
 }
 
-rlo_status rlo_ppo_gradient(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch,
-                            const rlo_logits* actor, const rlo_logits* old_logits, const rlo_logits* ref_logits,
-                            const float* old_logp, const float* ref_logp, const float* advantages,
-                            const rlo_token_out* out, void* stream) {
+}  // extern "C"
+
+namespace {
+
+// Validation (policy.cpp:315, :338-343, same order and messages) and the
+// VocabArgs of one loss pass; shared by rlo_ppo_gradient and the fused
+// update pass.  *empty = true for a batch without positions (nothing to do).
+rlo_status ppo_setup(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch, const rlo_logits* actor,
+                     const rlo_logits* old_logits, const rlo_logits* ref_logits, const float* old_logp,
+                     const float* ref_logp, const float* advantages, const rlo_token_out* out, cudaStream_t s,
+                     VocabArgs& a, bool* empty) {
+  *empty = true;
   if (!h) return fail(RLO_ERR_INPUT, "ppo_gradient: null handle");
   RLO_TRY(rlo_train_config_validate(cfg));  // policy.cpp:315
   RLO_TRY(check_batch(batch, "ppo_gradient", true));
   const int32_t B = batch->B, T = batch->T;
   const int64_t N = (int64_t)B * T;
   if (N == 0) return RLO_OK;
+  *empty = false;
   // policy.cpp:338-343, same order
   if (!advantages) return fail(RLO_ERR_INPUT, "ppo_gradient: sample '0' missing advantages");
   if (!old_logits && !old_logp) return fail(RLO_ERR_INPUT, "ppo_gradient: sample '0' missing old logprobs");
@@ -547,8 +562,6 @@ rlo_status rlo_ppo_gradient(rlo_handle* h, const rlo_train_config* cfg, const rl
   for (const rlo_logits* l : {old_logits, ref_logits})
     if (l && (l->dtype != actor->dtype || l->V != actor->V))
       return fail(RLO_ERR_INPUT, "ppo_gradient: actor/old/ref logits must share dtype and vocab size");
-  DeviceGuard g(h->device);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   RLO_CUDA(h->s_loss.ensure(N));
   RLO_CUDA(h->s_ratio.ensure(N));
   RLO_CUDA(h->s_kl.ensure(N));
@@ -569,7 +582,6 @@ rlo_status rlo_ppo_gradient(rlo_handle* h, const rlo_train_config* cfg, const rl
   }
   h->acc_nseq = std::max<int32_t>(h->acc_nseq, static_cast<int32_t>(need));
 
-  VocabArgs a;
   std::memset(&a, 0, sizeof(a));
   int nt = 0;
   auto add = [&](const rlo_logits* l, int role) {
@@ -612,7 +624,67 @@ rlo_status rlo_ppo_gradient(rlo_handle* h, const rlo_train_config* cfg, const rl
   a.s_ent = h->s_ent.p;
   a.s_flags = h->s_flags.p;
   a.err = h->err.p;
+  return RLO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+rlo_status rlo_ppo_gradient(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch,
+                            const rlo_logits* actor, const rlo_logits* old_logits, const rlo_logits* ref_logits,
+                            const float* old_logp, const float* ref_logp, const float* advantages,
+                            const rlo_token_out* out, void* stream) {
+  if (!h) return fail(RLO_ERR_INPUT, "ppo_gradient: null handle");
+  DeviceGuard g(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  VocabArgs a;
+  bool empty = true;
+  RLO_TRY(ppo_setup(h, cfg, batch, actor, old_logits, ref_logits, old_logp, ref_logp, advantages, out, s, a, &empty));
+  if (empty) return RLO_OK;
   RLO_CUDA(launch_vocab_loss(a, h->num_sms, s));
+  RLO_CUDA(launch_seq_reduce(batch->B, batch->T, batch->seq_offset, batch->lengths, batch->mask, h->s_loss.p,
+                             h->s_ratio.p, h->s_kl.p, h->s_ent.p, h->s_flags.p, h->recs.p, s));
+  return RLO_OK;
+}
+
+rlo_status rlo_ppo_gradient_fused(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch,
+                                  const rlo_logits* actor, const rlo_logits* old_logits, const rlo_logits* ref_logits,
+                                  const float* old_logp, const float* ref_logp, const float* advantages,
+                                  const float* weight, void* grad, int32_t grad_dtype, int64_t grad_row_stride,
+                                  const rlo_token_out* out, void* stream) {
+  if (!h) return fail(RLO_ERR_INPUT, "ppo_gradient: null handle");
+  if (batch && (int64_t)batch->B * batch->T > 0) {  // before any accumulator state changes
+    if (!weight || !grad) return fail(RLO_ERR_INPUT, "ppo_gradient_fused: weight and grad required");
+    if (grad_dtype != RLO_DTYPE_F32 && grad_dtype != RLO_DTYPE_BF16)
+      return fail(RLO_ERR_INPUT, "ppo_gradient_fused: unsupported grad dtype");
+    if (actor && grad_row_stride < actor->V) return fail(RLO_ERR_INPUT, "ppo_gradient_fused: grad row stride < V");
+  }
+  DeviceGuard g(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  VocabArgs a;
+  bool empty = true;
+  RLO_TRY(ppo_setup(h, cfg, batch, actor, old_logits, ref_logits, old_logp, ref_logp, advantages, out, s, a, &empty));
+  if (empty) return RLO_OK;
+  const int32_t B = batch->B, T = batch->T;
+  int32_t slice = 0;
+  const int K = getenv_flag("RLO_FUSED_OFF") ? 0 : fused_cluster_size(a, grad, grad_dtype, grad_row_stride, &slice);
+  cudaError_t e = K > 0 ? launch_vocab_fused(a, weight, grad, grad_dtype, grad_row_stride, K, slice, s)
+                        : cudaErrorNotSupported;
+  if (e != cudaSuccess) {
+    // not eligible (unaligned rows, vocab too large for a cluster's shared
+    // memory): the two-pass form, loss pass then backward epilogue
+    cudaGetLastError();
+    const int64_t N = (int64_t)B * T;
+    RLO_CUDA(h->s_lse.ensure(N));
+    RLO_CUDA(h->s_dlogp.ensure(N));
+    if (!a.o_lse) a.o_lse = h->s_lse.p;
+    if (!a.o_dlogp) a.o_dlogp = h->s_dlogp.p;
+    RLO_CUDA(launch_vocab_loss(a, h->num_sms, s));
+    RLO_CUDA(launch_logits_backward(actor->data, actor->dtype, actor->row_stride, actor->V, B, T, batch->lengths,
+                                    batch->tokens, a.o_lse, a.o_dlogp, weight, grad, grad_dtype, grad_row_stride,
+                                    h->num_sms, s));
+  }
   RLO_CUDA(launch_seq_reduce(B, T, batch->seq_offset, batch->lengths, batch->mask, h->s_loss.p, h->s_ratio.p,
                              h->s_kl.p, h->s_ent.p, h->s_flags.p, h->recs.p, s));
   return RLO_OK;
@@ -735,6 +807,40 @@ rlo_status rlo_objective_step_host(rlo_handle* h, const rlo_train_config* cfg, i
   if (host_logp_out && N)
     RLO_CUDA(cudaMemcpyAsync(host_logp_out, h->h_logp.p, sizeof(float) * N, cudaMemcpyDeviceToHost, s));
   return rlo_merge_gradients(h, cfg, stats, nullptr, stream);  // synchronises the stream
+}
+
+rlo_status rlo_batch_counts(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch, rlo_stats* out,
+                            void* stream) {
+  if (!h) return fail(RLO_ERR_INPUT, "batch_counts: null handle");
+  RLO_TRY(rlo_train_config_validate(cfg));
+  RLO_TRY(check_batch(batch, "batch_counts", false));
+  if (!out) return fail(RLO_ERR_INPUT, "batch_counts: out required");
+  std::memset(out, 0, sizeof(*out));
+  DeviceGuard g(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  RLO_CUDA(h->counts.ensure(static_cast<size_t>(batch->B > 0 ? batch->B : 1)));
+  RLO_CUDA(launch_batch_counts(batch->B, batch->T, cfg->group_size, batch->lengths, batch->mask, h->counts.p,
+                               h->stats4.p, s));
+  const double* src = h->stats4.p;
+  int world = 1;
+  if (h->comm) {  // global normalisers: all-gather, rank-ordered sum
+    RLO_NCCL(nccl_api().AllGather(h->stats4.p, h->stats_all.p, 4, ncclFloat64, h->comm, s));
+    src = h->stats_all.p;
+    world = h->world;
+  }
+  std::vector<double> host(static_cast<size_t>(4 * world));
+  RLO_CUDA(cudaMemcpyAsync(host.data(), src, sizeof(double) * host.size(), cudaMemcpyDeviceToHost, s));
+  RLO_CUDA(cudaStreamSynchronize(s));
+  double t = 0.0, q = 0.0, gr = 0.0;
+  for (int r = 0; r < world; ++r) {
+    t += host[4 * r + 0];
+    q += host[4 * r + 1];
+    gr += host[4 * r + 2];
+  }
+  out->tokens = static_cast<uint64_t>(t);
+  out->seqs = static_cast<uint64_t>(q);
+  out->groups = static_cast<uint64_t>(gr);
+  return RLO_OK;
 }
 
 rlo_status rlo_loss_weights(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch, const rlo_stats* stats,

@@ -10,6 +10,7 @@
 #include <cuda_bf16.h>
 
 #include "common.cuh"
+#include "grad_io.cuh"
 #include "internal.h"
 
 namespace rlo {
@@ -53,6 +54,37 @@ __global__ void loss_weight_kernel(int B, int T, int G, int agg, double tokens, 
   }
 }
 
+__global__ void __launch_bounds__(1024) count_reduce_kernel(int B, int G, const float* __restrict__ counts,
+                                                            double* __restrict__ out4) {
+  __shared__ double sm[3][32];
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    v[0] += (double)counts[b];
+    v[1] += counts[b] > 0.f ? 1.0 : 0.0;
+  }
+  for (int g0 = threadIdx.x * G; g0 < B; g0 += blockDim.x * G) {
+    float c = 0.f;
+    for (int b = g0; b < min(B, g0 + G); ++b) c += counts[b];
+    v[2] += c > 0.f ? 1.0 : 0.0;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    v[k] = warp_sum(v[k]);
+    if (lane == 0) sm[k][warp] = v[k];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      double x = lane < (int)(blockDim.x >> 5) ? sm[k][lane] : 0.0;
+      x = warp_sum(x);
+      if (lane == 0) out4[k] = x;
+    }
+    if (lane == 0) out4[3] = 0.0;
+  }
+}
+
 struct BwArgs {
   const void* logits;
   int64_t stride;
@@ -87,33 +119,6 @@ struct In<__nv_bfloat16> {
     for (int k = 0; k < 4; ++k) z[2 * k] = bf16lo(w[k]), z[2 * k + 1] = bf16hi(w[k]);
   }
   __device__ static float one(const __nv_bfloat16* p) { return __bfloat162float(*p); }
-};
-
-template <typename GT>
-struct Out;
-template <>
-struct Out<float> {
-  template <int N>
-  __device__ static void store(float* p, const float (&g)[8]) {
-    __stcs(reinterpret_cast<float4*>(p), make_float4(g[0], g[1], g[2], g[3]));
-    if (N == 8) __stcs(reinterpret_cast<float4*>(p) + 1, make_float4(g[4], g[5], g[6], g[7]));
-  }
-  __device__ static void one(float* p, float g) { p[0] = g; }
-};
-template <>
-struct Out<__nv_bfloat16> {
-  __device__ static uint32_t pack(float lo, float hi) {
-    return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(lo)) |
-           ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(hi)) << 16);
-  }
-  template <int N>
-  __device__ static void store(__nv_bfloat16* p, const float (&g)[8]) {
-    if (N == 8)
-      __stcs(reinterpret_cast<uint4*>(p), make_uint4(pack(g[0], g[1]), pack(g[2], g[3]), pack(g[4], g[5]), pack(g[6], g[7])));
-    else
-      __stcs(reinterpret_cast<uint2*>(p), make_uint2(pack(g[0], g[1]), pack(g[2], g[3])));
-  }
-  __device__ static void one(__nv_bfloat16* p, float g) { p[0] = __float2bfloat16_rn(g); }
 };
 
 template <typename ET, typename GT>
@@ -188,6 +193,14 @@ cudaError_t launch_loss_weights(int32_t B, int32_t T, int32_t G, int32_t agg, do
   loss_weight_kernel<<<(int)blocks, 256, 0, s>>>(B, T, G < 1 ? 1 : G, agg, tokens, seqs, groups, lengths, mask,
                                                  counts, w);
   g_launches.fetch_add(2, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_batch_counts(int32_t B, int32_t T, int32_t G, const int32_t* lengths, const uint8_t* mask,
+                                float* counts, double* out4, cudaStream_t s) {
+  if (B > 0) seq_count_kernel<<<(B + 7) / 8, 256, 0, s>>>(B, T, lengths, mask, counts);
+  count_reduce_kernel<<<1, 1024, 0, s>>>(B, G < 1 ? 1 : G, counts, out4);
+  g_launches.fetch_add(B > 0 ? 2 : 1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 

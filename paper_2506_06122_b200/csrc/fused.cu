@@ -1,0 +1,406 @@
+// fused.cu — the fused actor update pass: the loss part of ppo_gradient
+// (policy.cpp:355-374, a1-a9) and the actor backward epilogue
+// dlogits = w * dlogp * (onehot - softmax) (policy.cpp:375-379) in ONE read
+// of the actor logits.
+//
+// A thread-block cluster of K CTAs owns one row at a time.  CTA r streams the
+// slice [r*S, r*S + S) of the actor row with 128-bit LDG and keeps it in its
+// shared memory in a thread-private layout (vector j lives with thread
+// j mod 256, so no intra-CTA hazards), and streams the same slice of the
+// old-policy / reference rows without keeping them.  The K partial (mL, s, w)
+// states meet over DSMEM: one cluster barrier per row, double-buffered slots.
+// Every CTA combines the K partials in the same order (so all of them hold the
+// identical lse), runs the fp64 loss epilogue (the leader CTA writes the
+// per-token outputs and reduction scratch), and writes its gradient slice
+// straight from shared memory:
+//     g_v = -(w*dlp / s) * 2^(z_v*log2e - mL)   (+ w*dlp at the realised token)
+// where (mL, s) is the row's online state, so the softmax is neither stored
+// nor rebuilt from a rounded fp32 lse.
+//
+// HBM bytes per participating row: P*V*s_in + V*s_out, against
+// (P+1)*V*s_in + V*s_out for rlo_ppo_gradient followed by rlo_logits_backward.
+#include <cooperative_groups.h>
+
+#include <cstdio>
+#include <cstdlib>
+
+#include "grad_io.cuh"
+#include "vocab_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rlo {
+namespace vocab {
+namespace {
+
+constexpr int kFT = 256;
+constexpr int kFW = kFT / 32;
+
+struct FusedArgs {
+  VocabArgs v;
+  const float* weight;
+  void* grad;
+  int64_t gstride;
+  int32_t slice;  // elements per CTA slice (a multiple of the 16-byte vector width)
+};
+
+// This CTA's actor slice (n elements at src, 16-byte aligned).  LOAD: stream it
+// from HBM with U 128-bit loads in flight per thread and keep each vector in
+// shared memory; !LOAD: re-run the accumulation from shared memory (the
+// guarded entropy redo).  The sub-vector tail (last slice only) is read from
+// global memory both times.
+template <typename ET, int U, int MATHG, bool LOAD>
+__device__ __forceinline__ void slice_pass(const ET* __restrict__ src, int n, typename Vec<ET>::V* sm, Acc& a) {
+  using VT = Vec<ET>;
+  using VV = typename VT::V;
+  constexpr int kStep = kFT * U;
+  const int tid = threadIdx.x;
+  const int nvec = n / VT::kElems;
+  const int nfull = nvec / kStep * kStep;
+  const VV* __restrict__ vsrc = reinterpret_cast<const VV*>(src);
+  for (int base = 0; base < nfull; base += kStep) {
+    VV v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = LOAD ? ld_stream(vsrc + base + u * kFT + tid) : sm[base + u * kFT + tid];
+    if (LOAD) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) sm[base + u * kFT + tid] = v[u];
+    }
+    VT::template accumulate<U, true, MATHG>(v, a);
+  }
+  if (nfull < nvec) {
+    VV v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int idx = nfull + u * kFT + tid;
+      v[u] = idx < nvec ? (LOAD ? ld_stream(vsrc + idx) : sm[idx]) : VT::fill();
+      if (LOAD && idx < nvec) sm[idx] = v[u];
+    }
+    VT::template accumulate<U, true, MATHG>(v, a);
+  }
+  for (int i = nvec * VT::kElems + tid; i < n; i += kFT) {
+    const float z = VT::scalar(src + i);
+    acc_rescale<true>(a, z);
+    float w = 0.f, s = 0.f;
+    acc_elem<true>(z, a.mL, s, w);
+    a.s += s;
+    a.w += w;
+  }
+}
+
+template <typename ET>
+__device__ __forceinline__ void unpack(const typename Vec<ET>::V& v, float (&x)[8]);
+template <>
+__device__ __forceinline__ void unpack<float>(const float4& v, float (&x)[8]) {
+  x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void unpack<__nv_bfloat16>(const uint4& v, float (&x)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) x[2 * k] = bf16lo(w[k]), x[2 * k + 1] = bf16hi(w[k]);
+}
+
+// Gradient slice from shared memory: g = c * 2^(z*log2e - mL) (+ scale at the
+// token, tok_rel relative to the slice start).  scale == 0 writes zeros.
+template <typename ET, typename GT>
+__device__ __forceinline__ void slice_grad(const ET* __restrict__ src, int n, const typename Vec<ET>::V* sm,
+                                           GT* __restrict__ g, float mL, float c, int tok_rel, float scale) {
+  constexpr int E = Vec<ET>::kElems;
+  const int nvec = n / E;
+  if (scale == 0.f) {
+    float zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int j = threadIdx.x; j < nvec; j += kFT) Out<GT>::template store<E>(g + (int64_t)j * E, zero);
+    for (int i = nvec * E + threadIdx.x; i < n; i += kFT) Out<GT>::one(g + i, 0.f);
+    return;
+  }
+  for (int j = threadIdx.x; j < nvec; j += kFT) {  // exactly the vectors this thread stored
+    float x[8], o[8];
+    unpack<ET>(sm[j], x);
+#pragma unroll
+    for (int k = 0; k < E; ++k) o[k] = c * ex2(fmaf(x[k], kL2E, -mL));
+    const int d = tok_rel - j * E;
+    if (d >= 0 && d < E) {
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        if (k == d) o[k] += scale;
+    }
+    Out<GT>::template store<E>(g + (int64_t)j * E, o);
+  }
+  for (int i = nvec * E + threadIdx.x; i < n; i += kFT) {
+    float o = c * ex2(fmaf(Vec<ET>::scalar(src + i), kL2E, -mL));
+    if (i == tok_rel) o += scale;
+    Out<GT>::one(g + i, o);
+  }
+}
+
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
+constexpr int kEpiWarp = kFW;               // warp 8: the epilogue warp
+constexpr int kFTotal = kFT + 32;           // 8 streaming warps + the epilogue warp
+
+// Warp-specialised and software-pipelined over the cluster's rows.
+// Streaming warps 0-7, iteration i: stream row i (the actor slice into
+// shared-memory buffer i&1), deposit per-warp partials, then write the
+// gradient of row i-1 while the cluster barrier of row i completes.  The
+// epilogue warp, iteration i: gather the token logits of row i, combine the
+// warp partials into the CTA partial part[i&1], and after the cluster barrier
+// combine the peers' partials over DSMEM and run the fp64 epilogue (bc[i&1]),
+// while the streaming warps already stream row i+1.  So neither the barrier
+// nor the fp64 epilogue stalls the CTA's HBM stream.  Hazards: actor slices
+// and bc are double-buffered by iteration parity; part[i&1] is rewritten only
+// in iteration i+2, after every peer's epilogue warp has read it (its arrive
+// of iteration i+1 follows that read); only the epilogue warp writes part, so
+// only it arrives with release semantics.
+template <typename ET, typename GT, int NT, int U, int MATH>
+__global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
+  using VV = typename Vec<ET>::V;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ float part[2][NT][3];  // this CTA's partial state per tensor, read by the cluster over DSMEM
+  __shared__ float red[kFW][NT][3];
+  __shared__ float bc[2][4];  // per row: mL, -scale/s, scale, token offset in this slice
+  cg::cluster_group cl = cg::this_cluster();
+  const int K = (int)cl.num_blocks(), r = (int)cl.block_rank();
+  const VocabArgs& a = f.v;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool epi = warp == kEpiWarp;
+  const int64_t nrows = (int64_t)a.B * a.T;
+  const int64_t ncl = gridDim.x / K;
+  const int c0 = r * f.slice;
+  const int n = max(0, min(a.V - c0, f.slice));
+  VV* const smb0 = reinterpret_cast<VV*>(smraw);
+  VV* const smb1 = smb0 + f.slice / Vec<ET>::kElems;
+  // Next loss-participating row of this cluster at or after `row` (the same
+  // for every CTA of the cluster); rows passed over get their zero gradient
+  // slice (streaming warps) and inactive outputs here.
+  auto next_active = [&](int64_t row) {
+    for (; row < nrows; row += ncl) {
+      if (row_active<true>(a, row, r == 0 && tid == 0)) break;
+      if (r == 0 && tid == 0) write_inactive<true>(a, row);
+      if (!epi)
+        slice_grad<ET, GT>(nullptr, n, nullptr, reinterpret_cast<GT*>(f.grad) + row * f.gstride + c0, 0.f, 0.f, -1,
+                           0.f);
+    }
+    return row;
+  };
+  auto backward = [&](int64_t row, int b) {
+    const float* q = bc[b];
+    slice_grad<ET, GT>(reinterpret_cast<const ET*>(a.logits[0]) + row * a.stride[0] + c0, n, b ? smb1 : smb0,
+                       reinterpret_cast<GT*>(f.grad) + row * f.gstride + c0, q[0], q[1], __float_as_int(q[3]), q[2]);
+  };
+  int64_t prev = -1;
+  int b = 0;
+  for (int64_t row = next_active(blockIdx.x / K); row < nrows; row = next_active(row + ncl), b ^= 1) {
+    int tok = 0;
+    bool oov = false;
+    float ztok[NT];
+    if (epi) {
+      if (lane == 0) gather_token<ET, NT>(a, row, tok, oov, ztok);
+    } else {
+      VV* sm = b ? smb1 : smb0;
+      const ET* rp0 = reinterpret_cast<const ET*>(a.logits[0]) + row * a.stride[0] + c0;
+      Acc acc[NT];
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        acc_init(acc[k]);
+        if (k == 0) {
+          slice_pass<ET, U, MATH, true>(rp0, n, sm, acc[0]);
+          if (MATH != 0 && !(isfinite(acc[0].s) && isfinite(acc[0].w))) {
+            acc_init(acc[0]);  // -inf logits in this thread's share: redo it guarded, from shared memory
+            slice_pass<ET, U, MATH | kMathGuard, false>(rp0, n, sm, acc[0]);
+          }
+        } else {
+          const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + row * a.stride[k] + c0;
+          stream_accumulate<kFT, ET, U, false, false, MATH>(rp, n, true, acc[k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        if (k == 0)
+          acc_warp_reduce<true>(acc[k]);
+        else
+          acc_warp_reduce<false>(acc[k]);
+        if (lane == 0) {
+          red[warp][k][0] = acc[k].mL;
+          red[warp][k][1] = acc[k].s;
+          red[warp][k][2] = acc[k].w;
+        }
+      }
+    }
+    __syncthreads();  // red[] complete; bc[b^1] (row prev) visible
+    if (epi) {
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        Acc c;
+        if (lane < kFW) {
+          c.mL = red[lane][k][0];
+          c.s = red[lane][k][1];
+          c.w = red[lane][k][2];
+        } else {
+          acc_init(c);
+        }
+        if (k == 0)
+          acc_warp_reduce<true>(c);
+        else
+          acc_warp_reduce<false>(c);
+        if (lane == 0) {
+          part[b][k][0] = c.mL;
+          part[b][k][1] = c.s;
+          part[b][k][2] = c.w;
+        }
+      }
+      cluster_arrive_release();  // publish part[b]
+      cluster_wait();            // peers' part[b] visible
+      double lse[NT], ent = 0.0;
+      float mL0 = 0.f, s0 = 1.f;
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        Acc c;
+        if (lane < K) {
+          const float* p = cl.map_shared_rank(&part[b][k][0], lane);
+          c.mL = p[0];
+          c.s = p[1];
+          c.w = p[2];
+        } else {
+          acc_init(c);
+        }
+        if (k == 0)
+          acc_warp_reduce<true>(c);
+        else
+          acc_warp_reduce<false>(c);
+        const RowResult rr = finish(c);
+        lse[k] = rr.lse;
+        if (k == 0) {
+          ent = rr.entropy;
+          mL0 = c.mL;
+          s0 = c.s;
+        }
+      }
+      if (lane == 0) {
+        if (oov && r == 0) flag_error(a, DE_OOV_LOSS, tok);
+        const double nan = __longlong_as_double(0x7ff8000000000000LL);
+        double lp[NT];
+#pragma unroll
+        for (int k = 0; k < NT; ++k) lp[k] = oov ? nan : (double)ztok[k] - lse[k];
+        const double dlp = row_loss<NT>(a, row, lp, ent, lse[0], r == 0);
+        const float scale = __ldg(f.weight + row) * (float)dlp;
+        bc[b][0] = mL0;
+        bc[b][1] = (float)(-(double)scale / (double)s0);
+        bc[b][2] = scale;
+        bc[b][3] = __int_as_float(tok - c0);
+      }
+    } else {
+      cluster_arrive_relaxed();
+      if (prev >= 0) backward(prev, b ^ 1);  // overlaps the barrier and the epilogue
+      cluster_wait();
+    }
+    prev = row;
+  }
+  __syncthreads();  // the last row's bc
+  if (!epi && prev >= 0) backward(prev, b ^ 1);
+  cl.sync();  // DSMEM lifetime: no CTA exits while a peer may still read its slots
+}
+
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return (e && *e) ? std::atoi(e) : dflt;
+}
+
+template <typename ET, typename GT, int NT>
+cudaError_t launch_t(const FusedArgs& f, int K, cudaStream_t s) {
+  constexpr int U = sizeof(ET) == 4 ? 8 : 4;
+  constexpr int MATH = sizeof(ET) == 4 ? 1 : 4;  // the vocab pass's measured defaults
+  auto kern = fused_kernel<ET, GT, NT, U, MATH>;
+  const size_t smem = (size_t)f.slice * sizeof(ET) * 2;  // double-buffered actor slice
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = K;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(K);
+  cfg.blockDim = dim3(kFTotal);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  e = cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
+  if (e != cudaSuccess) return e;
+  if (ncl < 1) return cudaErrorInvalidConfiguration;
+  const int64_t nrows = (int64_t)f.v.B * f.v.T;
+  if (ncl > nrows) ncl = (int)nrows;
+  cfg.gridDim = dim3((unsigned)(ncl * K));
+  if (env_int("RLO_FUSED_DEBUG", 0))
+    fprintf(stderr, "[rlo] fused pass: K=%d slice=%d smem=%zu clusters=%d\n", K, f.slice, smem, ncl);
+  e = cudaLaunchKernelEx(&cfg, kern, f);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+template <typename ET, typename GT>
+cudaError_t launch_nt(const FusedArgs& f, int K, cudaStream_t s) {
+  switch (f.v.ntens) {
+    case 1: return launch_t<ET, GT, 1>(f, K, s);
+    case 2: return launch_t<ET, GT, 2>(f, K, s);
+    default: return launch_t<ET, GT, 3>(f, K, s);
+  }
+}
+
+}  // namespace
+}  // namespace vocab
+
+// Cluster size for a fused pass, or 0 when the two-pass form is used instead:
+// rows not 16-byte aligned, or an actor row that needs more than
+// kMaxCluster CTAs of the slice budget.  Measured (profiles/r1_fused.txt):
+// fp32 V=32000 runs best as 4 CTAs x 32 KB slices (3 CTAs/SM) and beats the
+// two-pass form by 14%; the bf16 Qwen row (304 KB) needs 8 CTAs of 38 KB and
+// loses to the two-pass form (the per-row cluster barrier couples 8 SMs), so
+// it stays two-pass.  RLO_FUSED_SLICE_KB overrides the budget (and then allows
+// clusters up to 8) for experiments.
+int fused_cluster_size(const VocabArgs& a, const void* grad, int32_t gdtype, int64_t gstride, int32_t* slice) {
+  const int esz = a.dtype == RLO_DTYPE_BF16 ? 2 : 4, gsz = gdtype == RLO_DTYPE_BF16 ? 2 : 4;
+  const int E = 16 / esz;
+  for (int k = 0; k < a.ntens; ++k)
+    if ((reinterpret_cast<uintptr_t>(a.logits[k]) & 15u) || ((a.stride[k] * esz) & 15)) return 0;
+  const int gal = E * gsz < 16 ? E * gsz : 16;  // widest gradient store
+  if ((reinterpret_cast<uintptr_t>(grad) % gal) || ((gstride * gsz) % gal)) return 0;
+  const int forced = vocab::env_int("RLO_FUSED_SLICE_KB", 0);
+  const int64_t budget = (int64_t)(forced > 0 ? forced : 32) * 1024;
+  const int kmax = forced > 0 ? 8 : 4;
+  for (int K = 1; K <= kmax; K *= 2) {
+    const int64_t per = ((int64_t)a.V + K - 1) / K;
+    const int64_t sl = (per + E - 1) / E * E;
+    if (sl * esz <= budget) {
+      *slice = (int32_t)sl;
+      return K;
+    }
+  }
+  return 0;
+}
+
+cudaError_t launch_vocab_fused(const VocabArgs& a, const float* weight, void* grad, int32_t gdtype, int64_t gstride,
+                               int K, int32_t slice, cudaStream_t s) {
+  using namespace vocab;
+  if ((int64_t)a.B * a.T == 0) return cudaSuccess;
+  FusedArgs f;
+  f.v = a;
+  f.weight = weight;
+  f.grad = grad;
+  f.gstride = gstride;
+  f.slice = slice;
+  if (a.dtype == RLO_DTYPE_BF16)
+    return gdtype == RLO_DTYPE_BF16 ? launch_nt<__nv_bfloat16, __nv_bfloat16>(f, K, s)
+                                    : launch_nt<__nv_bfloat16, float>(f, K, s);
+  return gdtype == RLO_DTYPE_BF16 ? launch_nt<float, __nv_bfloat16>(f, K, s) : launch_nt<float, float>(f, K, s);
+}
+
+}  // namespace rlo

@@ -128,6 +128,11 @@ struct AdvArgs {
 // Launchers (return cudaGetLastError()).
 cudaError_t launch_vocab_logprob(const VocabArgs& a, int num_sms, cudaStream_t s);
 cudaError_t launch_vocab_loss(const VocabArgs& a, int num_sms, cudaStream_t s);
+// Fused update pass (fused.cu): cluster size K (0 = not eligible) and the
+// per-CTA slice length, then the launch.
+int fused_cluster_size(const VocabArgs& a, const void* grad, int32_t gdtype, int64_t gstride, int32_t* slice);
+cudaError_t launch_vocab_fused(const VocabArgs& a, const float* weight, void* grad, int32_t gdtype, int64_t gstride,
+                               int K, int32_t slice, cudaStream_t s);
 cudaError_t launch_seq_reduce(int32_t B, int32_t T, int32_t seq_offset, const int32_t* lengths,
                               const uint8_t* mask, const float* s_loss, const float* s_ratio,
                               const float* s_kl, const float* s_ent, const uint8_t* s_flags, SeqRec* recs,
@@ -140,6 +145,10 @@ cudaError_t launch_whiten_clip(const AdvArgs& a, const double* stats_all, int32_
 cudaError_t launch_loss_weights(int32_t B, int32_t T, int32_t G, int32_t agg, double tokens, double seqs,
                                 double groups, const int32_t* lengths, const uint8_t* mask, float* counts, float* w,
                                 cudaStream_t s);
+// Loss-participating tokens, non-empty sequences and non-empty groups of a
+// batch -> out4[0..2] (fp64, exact integers); counts [B] scratch.
+cudaError_t launch_batch_counts(int32_t B, int32_t T, int32_t G, const int32_t* lengths, const uint8_t* mask,
+                                float* counts, double* out4, cudaStream_t s);
 cudaError_t launch_logits_backward(const void* logits, int32_t dtype, int64_t stride, int32_t V, int32_t B, int32_t T,
                                    const int32_t* lengths, const int32_t* tokens, const float* lse, const float* dlogp,
                                    const float* weight, void* grad, int32_t gdtype, int64_t gstride, int num_sms,

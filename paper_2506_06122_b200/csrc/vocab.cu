@@ -31,60 +31,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
-// PF: software prefetch — the next batch's U loads are issued before the
-// current batch's math, doubling the bytes in flight per thread.
-template <typename ET, int U, bool PF, bool ENT, int MATH>
-__device__ __forceinline__ void row_accumulate(const ET* __restrict__ row, int V, bool vec_ok, Acc& a) {
-  using VT = Vec<ET>;
-  using VV = typename VT::V;
-  constexpr int kStep = kThreads * U;
-  const int tid = threadIdx.x;
-  const int nvec = vec_ok ? V / VT::kElems : 0;
-  const int nfull = nvec / kStep * kStep;
-  const VV* __restrict__ vrow = reinterpret_cast<const VV*>(row) + tid;
-  if (PF) {
-    if (nfull > 0) {
-      VV cur[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) cur[u] = ld_stream(vrow + u * kThreads);
-      for (int base = kStep; base < nfull; base += kStep) {
-        VV nxt[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) nxt[u] = ld_stream(vrow + base + u * kThreads);
-        VT::template accumulate<U, ENT, MATH>(cur, a);
-#pragma unroll
-        for (int u = 0; u < U; ++u) cur[u] = nxt[u];
-      }
-      VT::template accumulate<U, ENT, MATH>(cur, a);
-    }
-  } else {
-    for (int base = 0; base < nfull; base += kStep) {  // full batches: unpredicated loads
-      VV v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = ld_stream(vrow + base + u * kThreads);
-      VT::template accumulate<U, ENT, MATH>(v, a);
-    }
-  }
-  if (nfull < nvec) {  // last partial batch
-    VV v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int idx = nfull + u * kThreads + tid;
-      v[u] = idx < nvec ? ld_stream(vrow - tid + idx) : VT::fill();
-    }
-    VT::template accumulate<U, ENT, MATH>(v, a);
-  }
-  // scalar tail (or the whole row when rows are not 16-byte aligned)
-  for (int i = nvec * VT::kElems + tid; i < V; i += kThreads) {
-    const float z = VT::scalar(row + i);
-    acc_rescale<ENT>(a, z);
-    float w = 0.f, s = 0.f;
-    acc_elem<ENT>(z, a.mL, s, w);
-    a.s += s;
-    if (ENT) a.w += w;
-  }
-}
-
 template <typename ET, int NT, int U, bool PF, bool LOSS, bool ENT0, int MATH>
 __global__ void __launch_bounds__(kThreads, 4) vocab_ldg_kernel(const VocabArgs a) {
   __shared__ float red[2][kWarps][NT][3];
@@ -111,15 +57,15 @@ __global__ void __launch_bounds__(kThreads, 4) vocab_ldg_kernel(const VocabArgs 
       acc_init(acc[k]);
       const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + row * a.stride[k];
       if (k == 0 && ENT0) {
-        row_accumulate<ET, U, PF, true, MATH>(rp, a.V, vec_ok, acc[k]);
+        stream_accumulate<kThreads, ET, U, PF, true, MATH>(rp, a.V, vec_ok, acc[k]);
         if (MATH != 0 && !(isfinite(acc[k].s) && isfinite(acc[k].w))) {
           // -inf logits in this thread's share: redo it with the entropy guard
           // (the row was just streamed, so the re-read hits L2)
           acc_init(acc[k]);
-          row_accumulate<ET, U, PF, true, MATH | kMathGuard>(rp, a.V, vec_ok, acc[k]);
+          stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, vec_ok, acc[k]);
         }
       } else
-        row_accumulate<ET, U, PF, false, MATH>(rp, a.V, vec_ok, acc[k]);
+        stream_accumulate<kThreads, ET, U, PF, false, MATH>(rp, a.V, vec_ok, acc[k]);
     }
 #pragma unroll
     for (int k = 0; k < NT; ++k) {

@@ -230,6 +230,61 @@ __device__ __forceinline__ float load_logit(const void* base, int64_t off) {
   return Vec<ET>::scalar(reinterpret_cast<const ET*>(base) + off);
 }
 
+// One row (or row slice) of V elements streamed by NTH threads with U 128-bit
+// loads in flight per thread.  PF: software prefetch — the next batch's U loads are issued before the
+// current batch's math, doubling the bytes in flight per thread.
+template <int NTH, typename ET, int U, bool PF, bool ENT, int MATH>
+__device__ __forceinline__ void stream_accumulate(const ET* __restrict__ row, int V, bool vec_ok, Acc& a) {
+  using VT = Vec<ET>;
+  using VV = typename VT::V;
+  constexpr int kStep = NTH * U;
+  const int tid = threadIdx.x;
+  const int nvec = vec_ok ? V / VT::kElems : 0;
+  const int nfull = nvec / kStep * kStep;
+  const VV* __restrict__ vrow = reinterpret_cast<const VV*>(row) + tid;
+  if (PF) {
+    if (nfull > 0) {
+      VV cur[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) cur[u] = ld_stream(vrow + u * NTH);
+      for (int base = kStep; base < nfull; base += kStep) {
+        VV nxt[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) nxt[u] = ld_stream(vrow + base + u * NTH);
+        VT::template accumulate<U, ENT, MATH>(cur, a);
+#pragma unroll
+        for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+      }
+      VT::template accumulate<U, ENT, MATH>(cur, a);
+    }
+  } else {
+    for (int base = 0; base < nfull; base += kStep) {  // full batches: unpredicated loads
+      VV v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld_stream(vrow + base + u * NTH);
+      VT::template accumulate<U, ENT, MATH>(v, a);
+    }
+  }
+  if (nfull < nvec) {  // last partial batch
+    VV v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int idx = nfull + u * NTH + tid;
+      v[u] = idx < nvec ? ld_stream(vrow - tid + idx) : VT::fill();
+    }
+    VT::template accumulate<U, ENT, MATH>(v, a);
+  }
+  // scalar tail (or the whole row when rows are not 16-byte aligned)
+  for (int i = nvec * VT::kElems + tid; i < V; i += NTH) {
+    const float z = VT::scalar(row + i);
+    acc_rescale<ENT>(a, z);
+    float w = 0.f, s = 0.f;
+    acc_elem<ENT>(z, a.mL, s, w);
+    a.s += s;
+    if (ENT) a.w += w;
+  }
+}
+
 struct RowResult {
   double lse;
   double entropy;
@@ -248,8 +303,10 @@ __device__ __forceinline__ void flag_error(const VocabArgs& a, int code, int val
 }
 
 // Loss epilogue for one loss-participating token (policy.cpp:355-374 + extensions), fp64.
-__device__ inline void loss_epilogue(const VocabArgs& a, int64_t row, double lp, double old, bool has_ref, double ref,
-                                     double ent, double lse) {
+// Returns dlogp; `write` = false computes it without touching the outputs (the
+// non-leader CTAs of a fused-pass cluster).
+__device__ inline double loss_epilogue(const VocabArgs& a, int64_t row, double lp, double old, bool has_ref, double ref,
+                                       double ent, double lse, bool write = true) {
   const double A = (double)a.adv[row];
   const double eps = a.clip_eps;
   const double ratio = exp(lp - old);                       // policy.cpp:358
@@ -290,6 +347,7 @@ __device__ inline void loss_epilogue(const VocabArgs& a, int64_t row, double lp,
   if (dual) flags |= TF_DUAL;
   if (!isfinite(dlp)) flags |= TF_NONFINITE_GRAD;
   if (!isfinite(loss)) flags |= TF_NONFINITE_LOSS;
+  if (!write) return dlp;
   a.s_loss[row] = (float)loss;
   a.s_ratio[row] = (float)ratio;
   a.s_kl[row] = has_ref ? (float)k : 0.f;
@@ -302,6 +360,33 @@ __device__ inline void loss_epilogue(const VocabArgs& a, int64_t row, double lp,
   if (a.o_dlogp) a.o_dlogp[row] = (float)dlp;
   if (a.o_loss) a.o_loss[row] = (float)loss;
   if (a.o_lse) a.o_lse[row] = (float)lse;
+  return dlp;
+}
+
+// Old/ref log-probs from the pass's own tensors (by role) or the caller's
+// precomputed arrays, then the loss epilogue.  Returns dlogp.
+template <int NT>
+__device__ __forceinline__ double row_loss(const VocabArgs& a, int64_t row, const double (&lp)[NT], double ent,
+                                           double lse0, bool write) {
+  double old = 0.0, ref = 0.0;
+  bool have_old = false, have_ref = false;
+#pragma unroll
+  for (int k = 1; k < NT; ++k) {
+    if (a.role[k] == ROLE_OLD) {
+      old = lp[k];
+      have_old = true;
+    }
+    if (a.role[k] == ROLE_REF) {
+      ref = lp[k];
+      have_ref = true;
+    }
+  }
+  if (!have_old) old = (double)a.old_lp_in[row];
+  if (!have_ref && a.ref_lp_in) {
+    ref = (double)a.ref_lp_in[row];
+    have_ref = true;
+  }
+  return loss_epilogue(a, row, lp[0], old, have_ref, ref, ent, lse0, write);
 }
 
 // Is `row` processed by this pass?  (forward_logprobs: every valid position;
@@ -381,25 +466,7 @@ __device__ __forceinline__ void row_finish(const VocabArgs& a, const float (*red
     if (a.out_tok) a.out_tok[row] = ztok[0];
     return;
   }
-  double old = 0.0, ref = 0.0;
-  bool have_old = false, have_ref = false;
-#pragma unroll
-  for (int k = 1; k < NT; ++k) {
-    if (a.role[k] == ROLE_OLD) {
-      old = lp[k];
-      have_old = true;
-    }
-    if (a.role[k] == ROLE_REF) {
-      ref = lp[k];
-      have_ref = true;
-    }
-  }
-  if (!have_old) old = (double)a.old_lp_in[row];
-  if (!have_ref && a.ref_lp_in) {
-    ref = (double)a.ref_lp_in[row];
-    have_ref = true;
-  }
-  loss_epilogue(a, row, lp[0], old, have_ref, ref, ent, lse[0]);
+  row_loss<NT>(a, row, lp, ent, lse[0], true);
 }
 
 }  // namespace vocab

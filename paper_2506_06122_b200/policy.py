@@ -312,6 +312,46 @@ class Objective:
                                           C.byref(st), _ptr(w), _stream(stream, self.device)))
         return w
 
+    def batch_counts(self, cfg: TrainConfig, lengths, T, mask=None, stream=None) -> "UpdateStats":
+        """Global token / sequence / group counts of a batch before its vocab
+        pass (the normalisers merge_gradients derives); feeds loss_weights
+        ahead of ppo_gradient_fused.  Synchronises."""
+        st = _abi.rlo_stats()
+        check(_abi.lib().rlo_batch_counts(self._h, C.byref(cfg.to_c()), C.byref(_batch(lengths, None, mask, T)),
+                                          C.byref(st), _stream(stream, self.device)))
+        return UpdateStats.from_c(st)
+
+    def ppo_gradient_fused(self, cfg: TrainConfig, tokens, lengths, actor_logits, advantages, weight, mask=None,
+                           old_logits=None, ref_logits=None, old_logprobs=None, ref_logprobs=None, seq_offset=0,
+                           grad=None, grad_dtype=None, outputs=("logp", "dlogp"), stream=None):
+        """ppo_gradient + the actor backward epilogue in one read of the actor
+        logits (policy.cpp:355-379).  Accumulates like ppo_gradient; returns
+        (per-token outputs dict, grad [B*T, V])."""
+        torch = _torch()
+        B, T = tokens.shape
+        _check_dev(tokens, torch.int32, "tokens")
+        _check_dev(lengths, torch.int32, "lengths")
+        _check_dev(mask, torch.uint8, "mask")
+        for t, n in ((advantages, "advantages"), (old_logprobs, "old_logprobs"), (ref_logprobs, "ref_logprobs"),
+                     (weight, "weight")):
+            _check_dev(t, torch.float32, n)
+        if grad is None:
+            grad = torch.empty(B * T, actor_logits.shape[-1], dtype=grad_dtype or actor_logits.dtype,
+                               device=actor_logits.device)
+        G = _logits(grad, "grad")
+        res = {k: torch.empty(B, T, dtype=torch.float32, device=tokens.device) for k in outputs}
+        o = _abi.rlo_token_out()
+        for k in ("logp", "old_logp", "ref_logp", "entropy", "dlogp", "loss", "lse"):
+            setattr(o, k, res[k].data_ptr() if k in res else None)
+        L_old, L_ref = _logits(old_logits, "old_logits"), _logits(ref_logits, "ref_logits")
+        check(_abi.lib().rlo_ppo_gradient_fused(
+            self._h, C.byref(cfg.to_c()), C.byref(_batch(lengths, tokens, mask, T, seq_offset)),
+            C.byref(_logits(actor_logits, "actor_logits")), C.byref(L_old) if L_old else None,
+            C.byref(L_ref) if L_ref else None, _ptr(old_logprobs), _ptr(ref_logprobs), _ptr(advantages),
+            _ptr(weight), C.c_void_p(grad.data_ptr()), G.dtype, G.row_stride, C.byref(o),
+            _stream(stream, self.device)))
+        return res, grad
+
     def logits_backward(self, tokens, lengths, logits, lse, dlogp, weight, grad=None, grad_dtype=None, stream=None):
         """Actor backward epilogue (policy.cpp:375-379): dL/dlogits rows
         w*dlogp*(onehot - softmax); returns the gradient tensor."""
