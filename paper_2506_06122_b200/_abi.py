@@ -137,7 +137,11 @@ def lib() -> C.CDLL:
         "rlo_synth_tokens": ([vp, i64, i32, u64, i64, i64, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
-        fn = getattr(L, name)
+        fn = getattr(L, name, None)
+        if fn is None and os.environ.get("RLO_LIB"):
+            continue  # an older A/B build (RLO_LIB) may predate an entry point
+        if fn is None:
+            raise ImportError(f"{LIB_PATH} does not export {name}: rebuild the library")
         fn.argtypes = args
         fn.restype = res
     _lib = L

@@ -46,9 +46,8 @@ struct FusedArgs {
 
 // This CTA's actor slice (n elements at src, 16-byte aligned).  LOAD: stream it
 // from HBM with U 128-bit loads in flight per thread and keep each vector in
-// shared memory; !LOAD: re-run the accumulation from shared memory (the
-// guarded entropy redo).  The sub-vector tail (last slice only) is read from
-// global memory both times.
+// shared memory; !LOAD: run the accumulation from shared memory.  The
+// sub-vector tail (last slice only) is read from global memory.
 template <typename ET, int U, int MATHG, bool LOAD>
 __device__ __forceinline__ void slice_pass(const ET* __restrict__ src, int n, typename Vec<ET>::V* sm, Acc& a) {
   using VT = Vec<ET>;
@@ -210,11 +209,7 @@ __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
       for (int k = 0; k < NT; ++k) {
         acc_init(acc[k]);
         if (k == 0) {
-          slice_pass<ET, U, MATH, true>(rp0, n, sm, acc[0]);
-          if (MATH != 0 && !(isfinite(acc[0].s) && isfinite(acc[0].w))) {
-            acc_init(acc[0]);  // -inf logits in this thread's share: redo it guarded, from shared memory
-            slice_pass<ET, U, MATH | kMathGuard, false>(rp0, n, sm, acc[0]);
-          }
+          slice_pass<ET, U, MATH | kMathGuard, true>(rp0, n, sm, acc[0]);  // entropy row: guarded (vocab_common.cuh)
         } else {
           const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + row * a.stride[k] + c0;
           stream_accumulate<kFT, ET, U, false, false, MATH>(rp, n, true, acc[k]);

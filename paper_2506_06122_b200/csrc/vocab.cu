@@ -31,8 +31,14 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
+// Build-time knob for A/B library builds (make EXTRA="-D..."):
+// RLO_LDG_MIN_BLOCKS = __launch_bounds__ minimum CTAs per SM (register cap).
+#ifndef RLO_LDG_MIN_BLOCKS
+#define RLO_LDG_MIN_BLOCKS 4
+#endif
+
 template <typename ET, int NT, int U, bool PF, bool LOSS, bool ENT0, int MATH>
-__global__ void __launch_bounds__(kThreads, 4) vocab_ldg_kernel(const VocabArgs a) {
+__global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel(const VocabArgs a) {
   __shared__ float red[2][kWarps][NT][3];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t nrows = (int64_t)a.B * a.T;
@@ -57,13 +63,9 @@ __global__ void __launch_bounds__(kThreads, 4) vocab_ldg_kernel(const VocabArgs 
       acc_init(acc[k]);
       const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + row * a.stride[k];
       if (k == 0 && ENT0) {
-        stream_accumulate<kThreads, ET, U, PF, true, MATH>(rp, a.V, vec_ok, acc[k]);
-        if (MATH != 0 && !(isfinite(acc[k].s) && isfinite(acc[k].w))) {
-          // -inf logits in this thread's share: redo it with the entropy guard
-          // (the row was just streamed, so the re-read hits L2)
-          acc_init(acc[k]);
-          stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, vec_ok, acc[k]);
-        }
+        // entropy row always guarded: the -inf padding of a partial batch
+        // (and masked vocabulary entries) must give e*t = 0, not 0 * -inf
+        stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, vec_ok, acc[k]);
       } else
         stream_accumulate<kThreads, ET, U, PF, false, MATH>(rp, a.V, vec_ok, acc[k]);
     }

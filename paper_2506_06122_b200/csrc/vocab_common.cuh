@@ -100,10 +100,11 @@ __host__ __device__ constexpr int poly_deg_ent(int math) { return math == 4 ? 4 
 constexpr int kMathMask = 0xff;
 constexpr int kMathGuard = 0x100;
 
-// GUARD (entropy row only): clamp t so that -inf logits give
-// e*t = 2^-126 * -126 (negligible) instead of 0 * -inf = NaN.  The fast path
-// runs unguarded and a thread whose entropy sum comes out non-finite redoes
-// its share of the row guarded (vocab.cu), so finite rows pay nothing.
+// GUARD (entropy row): clamp t so that -inf logits (masked vocabulary entries
+// and the -inf padding of a partial batch) give e*t = 2^-126 * -126
+// (negligible) instead of 0 * -inf = NaN.  Two FMNMX per element pair.  (An
+// unguarded fast path with a guarded redo on a non-finite sum was measured
+// 20-50% slower: the padding of every partial batch triggers the redo.)
 template <bool ENT, bool GUARD>
 __device__ __forceinline__ void pair2(float zl, float zh, f2 L2, f2 nmL, f2& s, f2& w, int poly) {
   const f2 t = ffma2(pk2(zl, zh), L2, nmL);
