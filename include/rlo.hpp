@@ -137,6 +137,30 @@ class Objective {
     check(rlo_rank_partials(h_, &cfg, &p, stream));
     return p;
   }
+  // Actor update (policy.cpp:375-379): counts ahead of the pass -> weights ->
+  // loss + backward epilogue in one read of the actor logits.
+  UpdateStats batch_counts(const TrainConfig& cfg, const rlo_batch& batch, void* stream = nullptr) {
+    UpdateStats st{};
+    check(rlo_batch_counts(h_, &cfg, &batch, &st, stream));
+    return st;
+  }
+  void loss_weights(const TrainConfig& cfg, const rlo_batch& batch, const UpdateStats& counts, float* w,
+                    void* stream = nullptr) {
+    check(rlo_loss_weights(h_, &cfg, &batch, &counts, w, stream));
+  }
+  void ppo_gradient_fused(const TrainConfig& cfg, const rlo_batch& batch, const rlo_logits& actor,
+                          const rlo_logits* old_logits, const rlo_logits* ref_logits, const float* old_logp,
+                          const float* ref_logp, const float* adv, const float* weight, void* grad,
+                          int32_t grad_dtype, int64_t grad_row_stride, const rlo_token_out* out = nullptr,
+                          void* stream = nullptr) {
+    check(rlo_ppo_gradient_fused(h_, &cfg, &batch, &actor, old_logits, ref_logits, old_logp, ref_logp, adv, weight,
+                                 grad, grad_dtype, grad_row_stride, out, stream));
+  }
+  void logits_backward(const rlo_batch& batch, const rlo_logits& logits, const float* lse, const float* dlogp,
+                       const float* weight, void* grad, int32_t grad_dtype, int64_t grad_row_stride,
+                       void* stream = nullptr) {
+    check(rlo_logits_backward(h_, &batch, &logits, lse, dlogp, weight, grad, grad_dtype, grad_row_stride, stream));
+  }
   void sync(void* stream = nullptr) { check(rlo_sync(h_, stream)); }
   rlo_handle* get() const { return h_; }
 
