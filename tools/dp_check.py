@@ -88,6 +88,40 @@ def main():
                   f"adv max err {a_err:.2e}, tokens {st.tokens}", flush=True)
             fails += not ok
             single.close()
+    # fused update pass: global counts (all-gathered) -> weights -> loss + dlogits
+    # in one read of the actor logits; shards' gradient rows == the single run's
+    cfg = cfgs["gae+whiten+seq-mean"]
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    Ls, Ms = d(lengths[b0:b0 + n]), d(mask[b0:b0 + n])
+    adv = obj.compute_advantages(cfg, Ls, T=T, mask=Ms, rewards=d(rt[b0:b0 + n]), values=d(vals[b0:b0 + n]))
+    cnt = obj.batch_counts(cfg, Ls, T, mask=Ms)
+    w = obj.loss_weights(cfg, Ls, cnt, T, mask=Ms)
+    rows = slice(b0 * T, (b0 + n) * T)
+    _, g = obj.ppo_gradient_fused(cfg, toks[b0:b0 + n].contiguous(), Ls, full[0][rows], adv, w, mask=Ms,
+                                  old_logits=full[1][rows], ref_logits=full[2][rows])
+    st = obj.merge_gradients(cfg)
+    gpad = torch.zeros(B * T, V, dtype=g.dtype, device=dev)
+    gpad[: n * T] = g
+    gathered = [torch.zeros_like(gpad) for _ in range(world)] if rank == 0 else None
+    dist.gather(gpad, gathered, dst=0)
+    counts = [None] * world
+    dist.all_gather_object(counts, n)
+    if rank == 0:
+        single = rlo.Objective(local)
+        adv1 = single.compute_advantages(cfg, d(lengths), T=T, mask=d(mask), rewards=d(rt), values=d(vals))
+        cnt1 = single.batch_counts(cfg, d(lengths), T, mask=d(mask))
+        w1 = single.loss_weights(cfg, d(lengths), cnt1, T, mask=d(mask))
+        _, g1 = single.ppo_gradient_fused(cfg, toks, d(lengths), full[0], adv1, w1, mask=d(mask),
+                                          old_logits=full[1], ref_logits=full[2])
+        st1 = single.merge_gradients(cfg)
+        g_dp = torch.cat([x[: c * T] for x, c in zip(gathered, counts)])
+        g_err = float((g_dp.float() - g1.float()).abs().max())
+        ok = (cnt.tokens, cnt.seqs, cnt.groups) == (cnt1.tokens, cnt1.seqs, cnt1.groups) and g_err <= 1e-6
+        ok &= abs(st.loss - st1.loss) <= 1e-9 * max(1.0, abs(st1.loss))
+        print(f"{'PASS' if ok else 'FAIL'} dp{world} fused update pass: counts {cnt.tokens}/{cnt.seqs}/{cnt.groups}, "
+              f"dlogits max err {g_err:.2e}, loss {st.loss:.12f} vs {st1.loss:.12f}", flush=True)
+        fails += not ok
+        single.close()
     # ModelUpdateGroup: bucketed broadcast, destinations bit-identical for every
     # bucket size (test_policy_workers.cpp:100-130's sync_params property)
     n_params = 1_000_003
