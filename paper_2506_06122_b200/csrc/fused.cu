@@ -209,7 +209,11 @@ __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
       for (int k = 0; k < NT; ++k) {
         acc_init(acc[k]);
         if (k == 0) {
-          slice_pass<ET, U, MATH | kMathGuard, true>(rp0, n, sm, acc[0]);  // entropy row: guarded (vocab_common.cuh)
+          slice_pass<ET, U, MATH, true>(rp0, n, sm, acc[0]);
+          if (!(isfinite(acc[0].s) && isfinite(acc[0].w))) {
+            acc_init(acc[0]);  // -inf logits in this thread's share: redo it guarded, from shared memory
+            slice_pass<ET, U, MATH | kMathGuard, false>(rp0, n, sm, acc[0]);
+          }
         } else {
           const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + row * a.stride[k] + c0;
           stream_accumulate<kFT, ET, U, false, false, MATH>(rp, n, true, acc[k]);

@@ -36,6 +36,11 @@ constexpr int kWarps = kThreads / 32;
 #ifndef RLO_LDG_MIN_BLOCKS
 #define RLO_LDG_MIN_BLOCKS 4
 #endif
+// RLO_ENT_GUARD_ALWAYS = 1: the entropy row always runs the guarded math
+// (no redo path).
+#ifndef RLO_ENT_GUARD_ALWAYS
+#define RLO_ENT_GUARD_ALWAYS 0
+#endif
 
 template <typename ET, int NT, int U, bool PF, bool LOSS, bool ENT0, int MATH>
 __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel(const VocabArgs a) {
@@ -63,9 +68,17 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
       acc_init(acc[k]);
       const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + row * a.stride[k];
       if (k == 0 && ENT0) {
-        // entropy row always guarded: the -inf padding of a partial batch
-        // (and masked vocabulary entries) must give e*t = 0, not 0 * -inf
-        stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, vec_ok, acc[k]);
+        if (RLO_ENT_GUARD_ALWAYS) {
+          stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, vec_ok, acc[k]);
+        } else {
+          stream_accumulate<kThreads, ET, U, PF, true, MATH>(rp, a.V, vec_ok, acc[k]);
+          if (!(isfinite(acc[k].s) && isfinite(acc[k].w))) {
+            // -inf logits in this thread's share: redo it guarded (the share
+            // was just streamed, so the re-read mostly hits L2)
+            acc_init(acc[k]);
+            stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, vec_ok, acc[k]);
+          }
+        }
       } else
         stream_accumulate<kThreads, ET, U, PF, false, MATH>(rp, a.V, vec_ok, acc[k]);
     }

@@ -100,11 +100,11 @@ __host__ __device__ constexpr int poly_deg_ent(int math) { return math == 4 ? 4 
 constexpr int kMathMask = 0xff;
 constexpr int kMathGuard = 0x100;
 
-// GUARD (entropy row): clamp t so that -inf logits (masked vocabulary entries
-// and the -inf padding of a partial batch) give e*t = 2^-126 * -126
-// (negligible) instead of 0 * -inf = NaN.  Two FMNMX per element pair.  (An
-// unguarded fast path with a guarded redo on a non-finite sum was measured
-// 20-50% slower: the padding of every partial batch triggers the redo.)
+// GUARD (entropy row): clamp t so that -inf logits (masked vocabulary
+// entries) give e*t = 2^-126 * -126 (negligible) instead of 0 * -inf = NaN.
+// Two FMNMX per element pair, so the entropy row runs unguarded and a thread
+// whose entropy sum comes out non-finite redoes its share guarded (vocab.cu,
+// fused.cu); the batch padding is finite (fill()) and never triggers it.
 template <bool ENT, bool GUARD>
 __device__ __forceinline__ void pair2(float zl, float zh, f2 L2, f2 nmL, f2& s, f2& w, int poly) {
   const f2 t = ffma2(pk2(zl, zh), L2, nmL);
@@ -132,8 +132,11 @@ template <>
 struct Vec<float> {
   using V = float4;
   static constexpr int kElems = 4;
-  // -inf padding contributes exp2(-inf) = 0 and never raises the running max.
-  __device__ static V fill() { return make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY); }
+  // Padding of a partial batch: -1e38 contributes 2^(-1.44e38) = 0, never
+  // raises the running max (init -1.44e30), and being finite keeps the
+  // unguarded entropy product e*t = 0*(-1.44e38) = 0 (a -inf pad would give
+  // NaN).  t stays finite: -1e38*log2e - m > -3.4e38.
+  __device__ static V fill() { return make_float4(-1e38f, -1e38f, -1e38f, -1e38f); }
   template <int U>
   __device__ static float chunk_max(const V (&v)[U]) {
     float m = fmaxf(fmaxf(v[0].x, v[0].y), fmaxf(v[0].z, v[0].w));
@@ -176,7 +179,7 @@ template <>
 struct Vec<__nv_bfloat16> {
   using V = uint4;
   static constexpr int kElems = 8;
-  __device__ static V fill() { return make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u); }  // -inf
+  __device__ static V fill() { return make_uint4(0xFE97FE97u, 0xFE97FE97u, 0xFE97FE97u, 0xFE97FE97u); }  // -1.004e38
   __device__ static __nv_bfloat162 as_b2(uint32_t x) { return *reinterpret_cast<__nv_bfloat162*>(&x); }
   template <int U>
   __device__ static float chunk_max(const V (&v)[U]) {
