@@ -6,17 +6,13 @@
 // "old" log-prob of the PPO ratio, so emitting it here removes the separate
 // old-policy logits pass (P = 3 -> 2).
 //
-// One CTA per row, 8 warps; warp j owns the contiguous token range
-// [j*W, (j+1)*W) (lane-strided inside, so loads stay coalesced).
-//   pass 1: per warp, online max + fp64 tempered sum sum exp((z-m)/T) and
-//           untempered sum sum exp(z-m) (fp64 exp: the reference's precision);
-//   combine: thread 0 rescales the warp sums to the row max in warp order,
-//           forms the row totals and the warp prefix, and finds the warp whose
-//           range holds the crossing of u * total;
-//   pass 2: that warp re-reads its range in 32-element chunks, warp prefix
-//           sums (shfl), and takes the first token whose cumulative tempered
-//           mass exceeds the threshold — the reference's first `u < acc`.
-// Traffic per row ~ (1 + 1/8) x V x s; latency-bound at decode batch sizes.
+// The tempered weights exp((z - m)/T) are fp64 (the reference's precision:
+// the CDF walk picks the same token unless u * total falls within fp64
+// rounding of a CDF boundary), through a table-driven exp (exp_neg); the
+// UNtempered log-sum-exp only feeds the returned log-prob and runs in fp32 in
+// log2 units like the vocab pass (relative error ~1e-7).
+// Traffic per row ~ (1 + 1/8) x V x s; bound by fp64 throughput (~13 fp64
+// operations per element).
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -47,73 +43,176 @@ __device__ __forceinline__ double keyed_double4(uint64_t a, uint64_t b, uint64_t
 }
 
 template <typename ET>
-__device__ __forceinline__ double logit(const ET* p, int v);
+__device__ __forceinline__ float logit(const ET* p, int v);
 template <>
-__device__ __forceinline__ double logit<float>(const float* p, int v) {
-  return (double)__ldg(p + v);
+__device__ __forceinline__ float logit<float>(const float* p, int v) {
+  return __ldg(p + v);
 }
 template <>
-__device__ __forceinline__ double logit<__nv_bfloat16>(const __nv_bfloat16* p, int v) {
-  return (double)__bfloat162float(p[v]);
+__device__ __forceinline__ float logit<__nv_bfloat16>(const __nv_bfloat16* p, int v) {
+  return __bfloat162float(p[v]);
 }
 
+// exp(t) for t <= 0 in fp64 (the reference's std::exp precision, <= 1 ulp):
+// t = (64k + j) ln2/64 + r, |r| <= ln2/128; exp(t) = 2^k * 2^(j/64) * e^r with
+// 2^(j/64) from a 64-entry shared table and e^r from a degree-5 Taylor
+// polynomial (truncation r^6/720 < 4e-17).  10 fp64 operations instead of the
+// ~20 of the library exp(); t < -708 is clamped (3e-308, below every sum it
+// enters).
+__device__ __forceinline__ double exp_neg(double t, const double* __restrict__ tab) {
+  t = fmax(t, -708.0);  // branch-free: exp(-708) = 3e-308 stands in for 0 (and for -inf logits)
+  constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round to integer
+  constexpr double k64Ln2 = 92.332482616893656;  // 64 / ln 2
+  constexpr double kLn2o64Hi = 0x1.62e42fefa0000p-7, kLn2o64Lo = 0x1.cf79abc9e3b3ap-46;
+  const double s = fma(t, k64Ln2, kMagic);
+  const int n = __double2loint(s);
+  const double nf = s - kMagic;
+  double r = fma(nf, -kLn2o64Hi, t);
+  r = fma(nf, -kLn2o64Lo, r);
+  double p = fma(r, 1.0 / 120, 1.0 / 24);
+  p = fma(p, r, 1.0 / 6);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double v = tab[n & 63] * p;
+  return __longlong_as_double(__double_as_longlong(v) + ((long long)(n >> 6) << 52));
+}
+
+template <typename ET>
+struct DVec;
+template <>
+struct DVec<float> {
+  static constexpr int E = 4;
+  __device__ static void load(const float* p, float (&x)[8]) {
+    const float4 v = ld_stream(reinterpret_cast<const float4*>(p));
+    x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
+  }
+};
+template <>
+struct DVec<__nv_bfloat16> {
+  static constexpr int E = 8;
+  __device__ static void load(const __nv_bfloat16* p, float (&x)[8]) {
+    const uint4 v = ld_stream(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[2 * k] = bf16lo(w[k]), x[2 * k + 1] = bf16hi(w[k]);
+  }
+};
+
+// Elements [v, v+E) of the row (fewer at the end of a range / the row):
+// vector load when the whole vector is inside and aligned, else per element;
+// missing elements -inf.
+template <typename ET>
+__device__ __forceinline__ void load_e(const ET* z, int v, int lim, bool vec_ok, float (&x)[8]) {
+  constexpr int E = DVec<ET>::E;
+  if (vec_ok && v + E <= lim) {
+    DVec<ET>::load(z + v, x);
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = v + e < lim ? logit(z, v + e) : -INFINITY;
+  }
+}
+
+// One CTA per row, 8 warps; warp j owns the contiguous token range
+// [j*W, (j+1)*W), W a multiple of 32*E; lane l takes the E consecutive tokens
+// at base + l*E of each 32*E step (16-byte loads, token order preserved).
+//   pass 1: per thread, running max m (exact: the logits are fp32/bf16), the
+//           fp64 tempered sum of exp((z - m)/T) (rescaled when m grows) and
+//           the fp32 untempered online sum (log2 units, as the vocab pass);
+//   combine: warp then block (warp order), thread 0 forms the totals, the
+//           keyed uniform u, X = u * total, and the warp whose range holds X;
+//   pass 2: the 8 warps sum 8 sub-ranges of the crossing range (weights
+//           relative to the row max); thread 0 picks the crossing sub-range;
+//           warp 0 walks it: per step each lane sums its E weights, a warp
+//           inclusive scan, the first lane whose prefix passes X walks its E
+//           tokens in order (the reference's first `u < acc`).
 template <typename ET>
 __global__ void __launch_bounds__(kDecWarps * 32)
     decode_kernel(const ET* __restrict__ logits, int64_t stride, int V, int n, double temp, uint64_t seed,
                   uint64_t version, const uint64_t* __restrict__ keys, const uint64_t* __restrict__ positions,
                   int32_t* __restrict__ out_tok, float* __restrict__ out_lp) {
-  __shared__ double s_m[kDecWarps], s_t[kDecWarps], s_u[kDecWarps];
-  __shared__ double s_base, s_thresh, s_m_row;
-  __shared__ int s_warp;
+  constexpr int E = DVec<ET>::E;
+  __shared__ double tab[64];
+  __shared__ double s_t[kDecWarps];
+  __shared__ float s_m[kDecWarps], s_ml[kDecWarps], s_su[kDecWarps];
+  __shared__ double s_base, s_thresh, s_lse;
+  __shared__ float s_M;
+  __shared__ int s_warp, s_pick;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int W = ((V + kDecWarps - 1) / kDecWarps + 31) / 32 * 32;
+  if (threadIdx.x < 64) tab[threadIdx.x] = exp2((double)threadIdx.x / 64.0);
+  __syncthreads();
+  const double inv_t = 1.0 / temp;
+  const bool unit_t = temp == 1.0;
+  const int W = ((V + kDecWarps - 1) / kDecWarps + 32 * E - 1) / (32 * E) * (32 * E);
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(logits) & 15u) == 0) && (((stride * (int64_t)sizeof(ET)) & 15) == 0);
   for (int row = blockIdx.x; row < n; row += gridDim.x) {
     const ET* z = logits + (int64_t)row * stride;
     const int v0 = warp * W, v1 = min(V, v0 + W);
-    // pass 1: online max + fp64 sums over the warp's range
-    double m = -INFINITY, st = 0.0, su = 0.0;
-    for (int v = v0 + lane; v < v1; v += 32) {
-      const double x = logit(z, v);
-      if (x > m) {
-        if (m != -INFINITY) {
-          st *= exp((m - x) / temp);
-          su *= exp(m - x);
-        }
-        m = x;
+    // pass 1
+    float m = -INFINITY, mL = kNegInit * kL2E, su = 0.f;
+    double st = 0.0;
+    for (int b = v0 + lane * E; b < v1; b += 32 * E) {
+      float x[8];
+      load_e<ET>(z, b, v1, vec_ok, x);
+      float cm = x[0];
+#pragma unroll
+      for (int e = 1; e < E; ++e) cm = fmaxf(cm, x[e]);
+      if (cm > m) {
+        if (m != -INFINITY) st *= exp_neg(unit_t ? (double)m - cm : ((double)m - cm) * inv_t, tab);
+        m = cm;
+        const float nmL = __fmul_rn(cm, kL2E);
+        su *= ex2(mL - nmL);
+        mL = nmL;
       }
-      st += exp((x - m) / temp);
-      su += exp(x - m);
+      if (m == -INFINITY) continue;
+      double w[8];
+      float q[8];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const double d = (double)x[e] - (double)m;
+        w[e] = exp_neg(unit_t ? d : d * inv_t, tab);
+        q[e] = ex2(fmaf(x[e], kL2E, -mL));  // -inf -> ex2(-inf) = 0
+      }
+#pragma unroll
+      for (int h = E / 2; h > 0; h >>= 1) {  // pairwise: no serial chain of fp64 adds
+#pragma unroll
+        for (int e = 0; e < h; ++e) w[e] += w[e + h], q[e] += q[e + h];
+      }
+      st += w[0];
+      su += q[0];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {  // warp combine (max, rescaled sums)
-      const double m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
       const double t2 = __shfl_xor_sync(0xffffffffu, st, o);
-      const double u2 = __shfl_xor_sync(0xffffffffu, su, o);
-      const double M = fmax(m, m2);
+      const float ml2 = __shfl_xor_sync(0xffffffffu, mL, o);
+      const float u2 = __shfl_xor_sync(0xffffffffu, su, o);
+      const float M = fmaxf(m, m2);
       if (M != -INFINITY) {
-        st = (m == -INFINITY ? 0.0 : st * exp((m - M) / temp)) + (m2 == -INFINITY ? 0.0 : t2 * exp((m2 - M) / temp));
-        su = (m == -INFINITY ? 0.0 : su * exp(m - M)) + (m2 == -INFINITY ? 0.0 : u2 * exp(m2 - M));
+        st = (m == -INFINITY ? 0.0 : st * exp_neg(unit_t ? (double)m - M : ((double)m - M) * inv_t, tab)) +
+             (m2 == -INFINITY ? 0.0 : t2 * exp_neg(unit_t ? (double)m2 - M : ((double)m2 - M) * inv_t, tab));
       }
+      const float ML = fmaxf(mL, ml2);
+      su = su * ex2(mL - ML) + u2 * ex2(ml2 - ML);
       m = M;
+      mL = ML;
     }
     if (lane == 0) {
       s_m[warp] = m;
       s_t[warp] = st;
-      s_u[warp] = su;
+      s_ml[warp] = mL;
+      s_su[warp] = su;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      double M = -INFINITY;
-      for (int j = 0; j < kDecWarps; ++j) M = fmax(M, s_m[j]);
+      float M = -INFINITY, ML = kNegInit * kL2E;
+      for (int j = 0; j < kDecWarps; ++j) M = fmaxf(M, s_m[j]), ML = fmaxf(ML, s_ml[j]);
       double T = 0.0, U = 0.0;
       for (int j = 0; j < kDecWarps; ++j) {
-        if (s_m[j] == -INFINITY) {
-          s_t[j] = 0.0;
-          continue;
-        }
-        s_t[j] *= exp((s_m[j] - M) / temp);
+        s_t[j] = s_m[j] == -INFINITY ? 0.0
+                                      : s_t[j] * exp_neg(unit_t ? (double)s_m[j] - M : ((double)s_m[j] - M) * inv_t, tab);
         T += s_t[j];
-        U += s_u[j] * exp(s_m[j] - M);
+        U += (double)s_su[j] * exp2((double)s_ml[j] - (double)ML);
       }
       const double u = keyed_double4(seed, version, keys[row], positions[row]);  // policy.cpp:158
       const double X = u * T;
@@ -129,40 +228,106 @@ __global__ void __launch_bounds__(kDecWarps * 32)
       s_warp = jw;
       s_base = base;
       s_thresh = X;
-      s_m_row = M;
-      s_u[0] = M + log(U);  // untempered lse (policy.cpp:117-121)
+      s_M = M;
+      s_lse = ((double)ML + log2(U)) / (double)kL2E;  // untempered lse (policy.cpp:117-121)
+      s_pick = V - 1;                                 // policy.cpp:160: no crossing -> last token
     }
     __syncthreads();
     const int jw = s_warp;
-    int chosen = V - 1;  // policy.cpp:160: no crossing -> last token
-    if (warp == jw) {
-      const double M = s_m_row, X = s_thresh;
-      double acc = s_base;
+    if (jw >= 0) {
+      // pass 2a: the 8 warps split the crossing warp's range into 8 sub-ranges
+      // and sum their weights (relative to the row max) in parallel
+      const double M = s_M;
       const int a0 = jw * W, a1 = min(V, a0 + W);
-      for (int c = a0; c < a1; c += 32) {
-        const int v = c + lane;
-        double p = v < a1 ? exp((logit(z, v) - M) / temp) : 0.0;
+      const int W2 = ((W + kDecWarps - 1) / kDecWarps + 32 * E - 1) / (32 * E) * (32 * E);
+      {
+        const int c0 = a0 + warp * W2, c1 = min(a1, c0 + W2);
+        double ls = 0.0;
+        for (int b = c0 + lane * E; b < c1; b += 32 * E) {
+          float x[8];
+          double w[8];
+          load_e<ET>(z, b, c1, vec_ok, x);
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {  // inclusive prefix
-          const double q = __shfl_up_sync(0xffffffffu, p, o);
-          if (lane >= o) p += q;
+          for (int e = 0; e < E; ++e) {
+            const double d = (double)x[e] - M;
+            w[e] = b + e < c1 ? exp_neg(unit_t ? d : d * inv_t, tab) : 0.0;
+          }
+#pragma unroll
+          for (int h = E / 2; h > 0; h >>= 1) {
+#pragma unroll
+            for (int e = 0; e < h; ++e) w[e] += w[e + h];
+          }
+          ls += w[0];
         }
-        const unsigned hit = __ballot_sync(0xffffffffu, v < a1 && X < acc + p);
-        if (hit) {
-          chosen = c + __ffs(hit) - 1;
-          break;
-        }
-        acc += __shfl_sync(0xffffffffu, p, 31);
+        ls = warp_sum(ls);
+        if (lane == 0) s_t[warp] = ls;  // pass 1's warp sums are no longer needed
       }
-      // a crossing placed in this warp by the rescaled totals but missed by the
-      // in-order prefix (rounding at a CDF boundary): the range's last token
-      if (lane == 0) s_warp = chosen == V - 1 ? a1 - 1 : chosen;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const double X = s_thresh;
+        double base = s_base;
+        int k = kDecWarps - 1;  // rounding between the rescaled totals and the sub-range sums: last sub-range
+        for (int j = 0; j < kDecWarps; ++j) {
+          if (X < base + s_t[j]) {
+            k = j;
+            break;
+          }
+          if (j < kDecWarps - 1) base += s_t[j];
+        }
+        s_warp = k;
+        s_base = base;
+      }
+      __syncthreads();
+      // pass 2b: one warp walks the crossing sub-range in token order
+      const int ks = s_warp;
+      if (warp == 0) {
+        const double X = s_thresh;
+        double acc = s_base;
+        const int c0 = min(a1, a0 + ks * W2), c1 = min(a1, c0 + W2);
+        int pick = -1;
+        for (int b0 = c0; b0 < c1 && pick < 0; b0 += 32 * E) {
+          const int b = b0 + lane * E;
+          float x[8];
+          double w[8], ls = 0.0;
+          load_e<ET>(z, b, c1, vec_ok, x);
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const double d = (double)x[e] - M;
+            w[e] = b + e < c1 ? exp_neg(unit_t ? d : d * inv_t, tab) : 0.0;
+            ls += w[e];
+          }
+          double incl = ls;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {  // inclusive prefix of the lane sums
+            const double q = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += q;
+          }
+          const unsigned hit = __ballot_sync(0xffffffffu, b < c1 && X < acc + incl);
+          if (hit) {
+            const int hl = __ffs(hit) - 1;
+            int c = min(b + E, c1) - 1;  // rounding between the lane sum and the in-order walk: lane's last token
+            double a = acc + incl - ls;  // exclusive prefix: the walk resumes at this lane's first token
+            for (int e = 0; e < E; ++e) {
+              a += w[e];
+              if (b + e < c1 && X < a) {
+                c = b + e;
+                break;
+              }
+            }
+            pick = __shfl_sync(0xffffffffu, c, hl);
+          }
+          acc += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        // a crossing placed here by the sums but missed by the in-order prefix
+        // (rounding at a CDF boundary): the sub-range's last token
+        if (lane == 0) s_pick = pick >= 0 ? pick : max(c0, c1 - 1);
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      chosen = jw < 0 ? V - 1 : s_warp;
-      out_tok[row] = chosen;
-      out_lp[row] = (float)(logit(z, chosen) - s_u[0]);  // untempered logp (policy.cpp:168)
+      const int c = s_pick;
+      out_tok[row] = c;
+      out_lp[row] = (float)((double)logit(z, c) - s_lse);  // untempered logp (policy.cpp:168)
     }
     __syncthreads();
   }

@@ -165,3 +165,30 @@ def test_decode_sample_batch_and_distribution(env):
     p /= p.sum()
     freq = np.bincount(tok, minlength=V) / n
     assert np.abs(freq - p).max() < 0.03
+
+
+@pytest.mark.parametrize("dt,V,pad", [("bf16", 152064, 0), ("f32", 32000, 0), ("f32", 50257, 3), ("bf16", 1001, 5)])
+def test_decode_sample_large_vocab_vs_oracle(env, dt, V, pad):
+    """Production vocabularies (vectorised path), odd V and padded unaligned
+    strides (scalar path), three temperatures, masked (-inf) entries: tokens
+    equal to the fp64 oracle's CDF walk, untempered logp within 1e-5."""
+    torch, rlo, obj = env
+    rng = np.random.default_rng(V)
+    n = 48
+    rows = (rng.standard_normal((n, V)) * 3).astype(np.float32)
+    rows[np.arange(n), rng.integers(0, V, n)] += 8.0
+    rows[:4, rng.integers(0, V, V // 3)] = -np.inf
+    tdt = torch.float32 if dt == "f32" else torch.bfloat16
+    full = torch.zeros(n, V + pad, dtype=tdt)
+    full[:, :V] = torch.from_numpy(rows).to(tdt)
+    x = full.cuda()[:, :V]
+    ref_rows = full[:, :V].float().numpy().astype(np.float64)
+    keys = rng.integers(0, 2**62, n).astype(np.int64)
+    pos = rng.integers(0, 4096, n).astype(np.int64)
+    for temp in (1.0, 0.7, 1.3):
+        tok, lp = obj.decode_sample(x, temp, 99, 5, dev(torch, keys), dev(torch, pos))
+        tok, lp = tok.cpu().numpy(), lp.cpu().numpy()
+        for i in range(n):
+            want, want_lp = O.decode_next(ref_rows[i], temp, 99, 5, int(keys[i]), int(pos[i]))
+            assert tok[i] == want, (temp, i)
+            assert abs(lp[i] - want_lp) <= 1e-5 * max(1.0, abs(want_lp)), (temp, i, lp[i], want_lp)

@@ -1,0 +1,148 @@
+"""Measurements of the SURVEY.md §8f rows around the path (one JSON line each):
+
+  decode     sampling-time log-probs (rlo_decode_sample, decode_next policy.cpp:143-169):
+             rows/s and the HBM rate of one pass over each row
+  value      critic value loss (rlo_value_loss, value_gradient policy.cpp:474-540): tokens/s
+  jsonl      SampleBatch JSONL ingestion (rlo_batch_from_jsonl) against the reference's own
+             SampleBatch::from_jsonl + validate (oracle/_ref, when built): MB/s of JSONL
+  broadcast  ModelUpdateGroup bucketed NCCL broadcast (rlo_broadcast_params), under torchrun
+             with >= 2 ranks: algorithm bandwidth per bucket size
+
+The actor backward epilogue (row 1) is measured by tools/bench_update.py.
+
+    python tools/bench_next.py [--only decode,value,jsonl]
+    python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tools/bench_next.py --only broadcast
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2506_06122_b200 as rlo  # noqa: E402
+
+
+def timed(fn, iters=5, warm=2):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def bench_decode(obj):
+    for rows, V, dt in ((4096, 152064, torch.bfloat16), (32768, 152064, torch.bfloat16), (32768, 32000, torch.float32)):
+        x = torch.empty(rows, V, dtype=dt, device="cuda")
+        rlo.synth_logits(x, seed=1, model=0)
+        keys = torch.arange(rows, dtype=torch.int64, device="cuda") * 7919
+        pos = torch.full((rows,), 17, dtype=torch.int64, device="cuda")
+        ms = timed(lambda: obj.decode_sample(x, 0.8, 42, 3, keys, pos))
+        byts = rows * V * x.element_size()
+        print(json.dumps({"row": "decode", "rows": rows, "V": V, "dtype": str(dt).split(".")[-1], "ms": ms,
+                          "rows_per_s": rows / ms * 1e3, "gbs_one_pass": byts / ms / 1e6,
+                          "note": "fp64 tempered CDF walk; bytes = one pass over each row"}), flush=True)
+        del x
+
+
+def bench_value(obj):
+    B, T = 256, 16384
+    g = torch.Generator(device="cuda").manual_seed(0)
+    v = torch.randn(B, T, device="cuda", generator=g)
+    vo = v + 0.1 * torch.randn(B, T, device="cuda", generator=g)
+    R = torch.randn(B, T, device="cuda", generator=g)
+    L = torch.full((B,), T, dtype=torch.int32, device="cuda")
+    ms = timed(lambda: obj.value_loss(L, v, R, old_values=vo, value_clip=0.2))
+    byts = B * T * (4 * 3 + 4)
+    print(json.dumps({"row": "value", "B": B, "T": T, "ms": ms, "tokens_per_s": B * T / ms * 1e3,
+                      "gbs": byts / ms / 1e6, "note": "includes the host sync of the stats"}), flush=True)
+
+
+def bench_jsonl():
+    import oracle as O
+    n = 512
+    if O.ref_available():
+        text = O.ref_batch_jsonl(5, n)
+        src = "reference SampleBatch::to_jsonl"
+    else:
+        rng = np.random.default_rng(5)
+        lines = []
+        for i in range(n):
+            T = int(rng.integers(64, 512))
+            lines.append(json.dumps({"prompt_id": f"p{i // 8}", "sample_id": f"s{i}", "prompt": [1, 2, 3],
+                                     "response_tokens": rng.integers(0, 32000, T).tolist(),
+                                     "response_logprobs": rng.uniform(-5, 0, T).tolist(),
+                                     "scalar_reward": float(rng.random())}))
+        text = "\n".join(lines)
+        src = "synthetic"
+    mb = len(text.encode()) / 1e6
+    t0 = time.perf_counter()
+    k = 0
+    while time.perf_counter() - t0 < 2.0:
+        rlo.batch_from_jsonl(text)
+        k += 1
+    ours = (time.perf_counter() - t0) / k
+    out = {"row": "jsonl", "samples": n, "mb": mb, "source": src, "ms": ours * 1e3, "mb_per_s": mb / ours}
+    if O.ref_available():
+        t0 = time.perf_counter()
+        k = 0
+        while time.perf_counter() - t0 < 2.0:
+            O.ref_parse_validate_jsonl(text)
+            k += 1
+        ref = (time.perf_counter() - t0) / k
+        out.update(reference_ms=ref * 1e3, reference_mb_per_s=mb / ref, speedup=ref / ours)
+    print(json.dumps(out), flush=True)
+
+
+def bench_broadcast():
+    import torch.distributed as dist
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    obj = rlo.Objective(local)
+    uid = [rlo.Objective.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    obj.init_comm(uid[0], rank, world)
+    buf = torch.ones(1 << 28, dtype=torch.float32, device="cuda")  # 1 GiB of parameters
+    nbytes = buf.numel() * 4
+    for bucket in (1 << 22, 1 << 26, 1 << 28, nbytes):
+        dist.barrier()
+        ms = timed(lambda: obj.broadcast_params(buf, bucket_bytes=bucket, root=0), iters=5, warm=2)
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            print(json.dumps({"row": "broadcast", "world": world, "bytes": nbytes, "bucket_bytes": bucket,
+                              "ms": float(t.item()), "algbw_gbs": nbytes / float(t.item()) / 1e6}), flush=True)
+    obj.close()
+    dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="decode,value,jsonl")
+    args = ap.parse_args()
+    rows = args.only.split(",")
+    if "broadcast" in rows:
+        bench_broadcast()
+        return
+    obj = rlo.Objective(0)
+    if "decode" in rows:
+        bench_decode(obj)
+    if "value" in rows:
+        bench_value(obj)
+    if "jsonl" in rows:
+        bench_jsonl()
+
+
+if __name__ == "__main__":
+    main()
