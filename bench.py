@@ -253,6 +253,7 @@ def run_ours(args, c):
                    "parallelism": f"dp{world}"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic_from_profile(args.config), "peak_kind": peak_kind,
+                     "frac_of_spec_8000": achieved / 8000.0,
                      "kernel": "vocab_kernel (fused 3-tensor logprob+entropy+loss pass, incl. per-seq reduce)",
                      "bytes_per_launch": bytes_per_launch, "avg_launch_ms": vocab_avg_ms},
         "e2e": e2e,
