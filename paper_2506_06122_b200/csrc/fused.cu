@@ -144,25 +144,52 @@ __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.w
 constexpr int kEpiWarp = kFW;               // warp 8: the epilogue warp
 constexpr int kFTotal = kFT + 32;           // 8 streaming warps + the epilogue warp
 
+// Named barriers (ids 1-4; 0 is __syncthreads), by iteration parity: RED =
+// "per-warp partials of row i are in red[i&1]" (streaming warps arrive, the
+// epilogue warp syncs); BC = "the epilogue of row i is in bc[i&1]" (the
+// epilogue warp arrives, the streaming warps sync).
+template <int ID>
+__device__ __forceinline__ void bar_arrive_id() { asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(kFTotal) : "memory"); }
+template <int ID>
+__device__ __forceinline__ void bar_sync_id() { asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(kFTotal) : "memory"); }
+constexpr int kBarRed = 1, kBarBc = 3;
+// immediate barrier ids (a register id makes ptxas reserve all 16)
+__device__ __forceinline__ void bar_arrive(int id) {
+  if (id == 1) bar_arrive_id<1>();
+  else if (id == 2) bar_arrive_id<2>();
+  else if (id == 3) bar_arrive_id<3>();
+  else bar_arrive_id<4>();
+}
+__device__ __forceinline__ void bar_sync(int id) {
+  if (id == 1) bar_sync_id<1>();
+  else if (id == 2) bar_sync_id<2>();
+  else if (id == 3) bar_sync_id<3>();
+  else bar_sync_id<4>();
+}
+
 // Warp-specialised and software-pipelined over the cluster's rows.
 // Streaming warps 0-7, iteration i: stream row i (the actor slice into
-// shared-memory buffer i&1), deposit per-warp partials, then write the
-// gradient of row i-1 while the cluster barrier of row i completes.  The
-// epilogue warp, iteration i: gather the token logits of row i, combine the
-// warp partials into the CTA partial part[i&1], and after the cluster barrier
-// combine the peers' partials over DSMEM and run the fp64 epilogue (bc[i&1]),
-// while the streaming warps already stream row i+1.  So neither the barrier
-// nor the fp64 epilogue stalls the CTA's HBM stream.  Hazards: actor slices
-// and bc are double-buffered by iteration parity; part[i&1] is rewritten only
-// in iteration i+2, after every peer's epilogue warp has read it (its arrive
-// of iteration i+1 follows that read); only the epilogue warp writes part, so
-// only it arrives with release semantics.
+// shared-memory buffer i&1), deposit per-warp partials (arrive RED), move
+// through the cluster barrier (wait for phase i-1, arrive for phase i), then
+// take row i-1's epilogue (sync BC) and write its gradient from buffer
+// (i-1)&1.  The epilogue warp, iteration i: gather row i's token logits, take
+// the partials (sync RED), publish the CTA partial part[i&1] over DSMEM,
+// arrive + wait at the cluster barrier, combine the K partials in rank order,
+// run the fp64 epilogue into bc[i&1] (arrive BC).  The streaming warps never
+// wait on the epilogue of the row they just streamed, and wait for the
+// cluster only one phase late, so a slower peer or a long epilogue costs
+// nothing unless it falls a whole row behind.  Hazards: red, bc and the actor
+// slices are double-buffered by parity and each is rewritten two iterations
+// later, after the consumer's next hand-off; part[i&1] is rewritten in
+// iteration i+2 only after every peer's epilogue warp has arrived for phase
+// i+1, i.e. after it read phase i's slots.  Only the epilogue warp writes
+// part, so only it arrives with release semantics.
 template <typename ET, typename GT, int NT, int U, int MATH>
 __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
   using VV = typename Vec<ET>::V;
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ float part[2][NT][3];  // this CTA's partial state per tensor, read by the cluster over DSMEM
-  __shared__ float red[kFW][NT][3];
+  __shared__ float red[2][kFW][NT][3];
   __shared__ float bc[2][4];  // per row: mL, -scale/s, scale, token offset in this slice
   cg::cluster_group cl = cg::this_cluster();
   const int K = (int)cl.num_blocks(), r = (int)cl.block_rank();
@@ -196,12 +223,7 @@ __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
   int64_t prev = -1;
   int b = 0;
   for (int64_t row = next_active(blockIdx.x / K); row < nrows; row = next_active(row + ncl), b ^= 1) {
-    int tok = 0;
-    bool oov = false;
-    float ztok[NT];
-    if (epi) {
-      if (lane == 0) gather_token<ET, NT>(a, row, tok, oov, ztok);
-    } else {
+    if (!epi) {
       VV* sm = b ? smb1 : smb0;
       const ET* rp0 = reinterpret_cast<const ET*>(a.logits[0]) + row * a.stride[0] + c0;
       Acc acc[NT];
@@ -226,21 +248,31 @@ __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
         else
           acc_warp_reduce<false>(acc[k]);
         if (lane == 0) {
-          red[warp][k][0] = acc[k].mL;
-          red[warp][k][1] = acc[k].s;
-          red[warp][k][2] = acc[k].w;
+          red[b][warp][k][0] = acc[k].mL;
+          red[b][warp][k][1] = acc[k].s;
+          red[b][warp][k][2] = acc[k].w;
         }
       }
-    }
-    __syncthreads();  // red[] complete; bc[b^1] (row prev) visible
-    if (epi) {
+      bar_arrive(kBarRed + b);
+      if (prev >= 0) cluster_wait();  // phase of row prev (one phase of slack)
+      cluster_arrive_relaxed();        // phase of row `row`
+      if (prev >= 0) {
+        bar_sync(kBarBc + (b ^ 1));  // row prev's epilogue
+        backward(prev, b ^ 1);
+      }
+    } else {
+      int tok = 0;
+      bool oov = false;
+      float ztok[NT];
+      if (lane == 0) gather_token<ET, NT>(a, row, tok, oov, ztok);
+      bar_sync(kBarRed + b);
 #pragma unroll
       for (int k = 0; k < NT; ++k) {
         Acc c;
         if (lane < kFW) {
-          c.mL = red[lane][k][0];
-          c.s = red[lane][k][1];
-          c.w = red[lane][k][2];
+          c.mL = red[b][lane][k][0];
+          c.s = red[b][lane][k][1];
+          c.w = red[b][lane][k][2];
         } else {
           acc_init(c);
         }
@@ -294,15 +326,16 @@ __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
         bc[b][2] = scale;
         bc[b][3] = __int_as_float(tok - c0);
       }
-    } else {
-      cluster_arrive_relaxed();
-      if (prev >= 0) backward(prev, b ^ 1);  // overlaps the barrier and the epilogue
-      cluster_wait();
+      __syncwarp();
+      bar_arrive(kBarBc + b);
     }
     prev = row;
   }
-  __syncthreads();  // the last row's bc
-  if (!epi && prev >= 0) backward(prev, b ^ 1);
+  if (!epi && prev >= 0) {
+    cluster_wait();  // the last phase
+    bar_sync(kBarBc + (b ^ 1));
+    backward(prev, b ^ 1);
+  }
   cl.sync();  // DSMEM lifetime: no CTA exits while a peer may still read its slots
 }
 
