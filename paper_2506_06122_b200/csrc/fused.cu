@@ -33,6 +33,11 @@ namespace rlo {
 namespace vocab {
 namespace {
 
+// A/B build knob: software prefetch in the old/ref streams (make EXTRA=-DRLO_FUSED_PF=1).
+#ifndef RLO_FUSED_PF
+#define RLO_FUSED_PF 0
+#endif
+
 constexpr int kFT = 256;
 constexpr int kFW = kFT / 32;
 
@@ -238,7 +243,7 @@ __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
           }
         } else {
           const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + row * a.stride[k] + c0;
-          stream_accumulate<kFT, ET, U, false, false, MATH>(rp, n, true, acc[k]);
+          stream_accumulate<kFT, ET, U, RLO_FUSED_PF != 0, false, MATH>(rp, n, true, acc[k]);
         }
       }
 #pragma unroll
