@@ -39,7 +39,7 @@ extern "C" {
 #pragma GCC visibility push(default) /* the library is built -fvisibility=hidden; export exactly this header */
 #endif
 
-#define RLO_ABI_VERSION 1
+#define RLO_ABI_VERSION 2
 
 /* Status codes — reference exception taxonomy (include/rollmini/errors.hpp). */
 typedef enum rlo_status {
@@ -106,12 +106,18 @@ typedef struct rlo_batch {
   const uint8_t* mask;     /* [B*T] device or NULL: action_mask (sample.hpp:26) */
 } rlo_batch;
 
-/* One model's logits over the batch rows. */
+/* One model's logits over the batch rows.  Padded layout (seq_start NULL):
+ * token (b, t) is row b*T + t.  Packed / varlen layout: token (b, t) is row
+ * seq_start[b] + t (e.g. cu_seqlens[b] of a [sum(lengths), V] tensor), only
+ * rows t < lengths[b] exist and are read or written — the logits of a
+ * ragged batch need no padding rows.  The per-token arrays of rlo_batch /
+ * rlo_token_out stay [B*T]. */
 typedef struct rlo_logits {
-  const void* data;        /* device; dtype elements */
-  int32_t dtype;           /* rlo_dtype */
-  int32_t V;               /* vocab size */
-  int64_t row_stride;      /* elements between consecutive rows (>= V) */
+  const void* data;          /* device; dtype elements */
+  int32_t dtype;             /* rlo_dtype */
+  int32_t V;                 /* vocab size */
+  int64_t row_stride;        /* elements between consecutive rows (>= V) */
+  const int64_t* seq_start;  /* device [B] or NULL (padded) */
 } rlo_logits;
 
 /* Optional per-token outputs of rlo_ppo_gradient ([B*T] device, any may be NULL). */

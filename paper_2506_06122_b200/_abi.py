@@ -14,6 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # RLO_LIB overrides the in-tree library (A/B builds of the same sources in kernel experiments).
 LIB_PATH = os.environ.get("RLO_LIB") or os.path.join(HERE, "lib", "librlo.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "rlo.h")
+ABI_VERSION = 2  # include/rlo.h RLO_ABI_VERSION: the struct layouts below
 
 RLO_OK, RLO_ERR_INPUT, RLO_ERR_CONFIG, RLO_ERR_TRAINING, RLO_ERR_CUDA, RLO_ERR_NCCL, RLO_ERR_DISPATCH = range(7)
 DTYPE_F32, DTYPE_BF16 = 0, 1
@@ -39,7 +40,8 @@ class rlo_batch(C.Structure):
 
 
 class rlo_logits(C.Structure):
-    _fields_ = [("data", C.c_void_p), ("dtype", C.c_int32), ("V", C.c_int32), ("row_stride", C.c_int64)]
+    _fields_ = [("data", C.c_void_p), ("dtype", C.c_int32), ("V", C.c_int32), ("row_stride", C.c_int64),
+                ("seq_start", C.c_void_p)]
 
 
 class rlo_token_out(C.Structure):
@@ -144,5 +146,8 @@ def lib() -> C.CDLL:
             raise ImportError(f"{LIB_PATH} does not export {name}: rebuild the library")
         fn.argtypes = args
         fn.restype = res
+    if L.rlo_abi_version() != ABI_VERSION and not os.environ.get("RLO_LIB"):
+        raise ImportError(f"{LIB_PATH} has ABI version {L.rlo_abi_version()}, this binding expects {ABI_VERSION}: "
+                          "rebuild the library")
     _lib = L
     return L

@@ -457,6 +457,7 @@ rlo_status rlo_forward_logprobs(rlo_handle* h, const rlo_batch* batch, const rlo
   std::memset(&a, 0, sizeof(a));
   a.logits[0] = logits->data;
   a.stride[0] = logits->row_stride;
+  a.seq_start[0] = logits->seq_start;
   a.role[0] = ROLE_ACTOR;
   a.ntens = 1;
   a.dtype = logits->dtype;
@@ -587,6 +588,7 @@ rlo_status ppo_setup(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch
   auto add = [&](const rlo_logits* l, int role) {
     a.logits[nt] = l->data;
     a.stride[nt] = l->row_stride;
+    a.seq_start[nt] = l->seq_start;
     a.role[nt] = role;
     ++nt;
   };
@@ -681,7 +683,8 @@ rlo_status rlo_ppo_gradient_fused(rlo_handle* h, const rlo_train_config* cfg, co
     if (!a.o_lse) a.o_lse = h->s_lse.p;
     if (!a.o_dlogp) a.o_dlogp = h->s_dlogp.p;
     RLO_CUDA(launch_vocab_loss(a, h->num_sms, s));
-    RLO_CUDA(launch_logits_backward(actor->data, actor->dtype, actor->row_stride, actor->V, B, T, batch->lengths,
+    RLO_CUDA(launch_logits_backward(actor->data, actor->dtype, actor->row_stride, actor->seq_start, actor->V, B, T,
+                                    batch->lengths,
                                     batch->tokens, a.o_lse, a.o_dlogp, weight, grad, grad_dtype, grad_row_stride,
                                     h->num_sms, s));
   }
@@ -870,7 +873,8 @@ rlo_status rlo_logits_backward(rlo_handle* h, const rlo_batch* batch, const rlo_
     return fail(RLO_ERR_INPUT, "logits_backward: unsupported grad dtype");
   if (grad_row_stride < logits->V) return fail(RLO_ERR_INPUT, "logits_backward: grad row stride < V");
   DeviceGuard g(h->device);
-  RLO_CUDA(launch_logits_backward(logits->data, logits->dtype, logits->row_stride, logits->V, batch->B, batch->T,
+  RLO_CUDA(launch_logits_backward(logits->data, logits->dtype, logits->row_stride, logits->seq_start, logits->V,
+                                  batch->B, batch->T,
                                   batch->lengths, batch->tokens, lse, dlogp, weight, grad, grad_dtype, grad_row_stride,
                                   h->num_sms, static_cast<cudaStream_t>(stream)));
   return RLO_OK;
@@ -919,6 +923,7 @@ rlo_status rlo_decode_sample(rlo_handle* h, const rlo_logits* logits, int32_t n_
   if (n_rows < 0) return fail(RLO_ERR_INPUT, "decode: negative row count");
   if (n_rows == 0) return RLO_OK;
   RLO_TRY(check_logits(logits, "decode", "policy"));
+  if (logits->seq_start) return fail(RLO_ERR_INPUT, "decode: rows are consecutive (seq_start must be NULL)");
   if (!sample_keys || !positions || !out_tokens || !out_logp)
     return fail(RLO_ERR_INPUT, "decode: sample_keys, positions, out_tokens and out_logp are required");
   DeviceGuard g(h->device);

@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(1024) count_reduce_kernel(int B, int G, const 
 struct BwArgs {
   const void* logits;
   int64_t stride;
+  const int64_t* seq_start;  // packed logits / gradient rows (NULL = padded)
   int32_t V, B, T;
   const int32_t* lengths;
   const int32_t* tokens;
@@ -129,9 +130,11 @@ __global__ void __launch_bounds__(kBwThreads) logits_backward_kernel(const BwArg
   for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
     const int b = (int)(row / a.T), t = (int)(row - (int64_t)b * a.T);
     const bool valid = t < seq_len(a.lengths, b, a.T);
+    if (a.seq_start && !valid) continue;  // packed: no such row
     const float scale = valid ? __ldg(a.weight + row) * __ldg(a.dlogp + row) : 0.f;
-    GT* g = reinterpret_cast<GT*>(a.grad) + row * a.gstride;
-    const ET* z = reinterpret_cast<const ET*>(a.logits) + row * a.stride;
+    const int64_t lrow = a.seq_start ? __ldg(a.seq_start + b) + t : row;
+    GT* g = reinterpret_cast<GT*>(a.grad) + lrow * a.gstride;
+    const ET* z = reinterpret_cast<const ET*>(a.logits) + lrow * a.stride;
     if (scale == 0.f) {  // non-participating (or zero-gradient) row: zeros
       float zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       for (int i = threadIdx.x; i < nvec; i += kBwThreads) Out<GT>::template store<N>(g + (int64_t)i * N, zero);
@@ -204,11 +207,12 @@ cudaError_t launch_batch_counts(int32_t B, int32_t T, int32_t G, const int32_t* 
   return cudaGetLastError();
 }
 
-cudaError_t launch_logits_backward(const void* logits, int32_t dtype, int64_t stride, int32_t V, int32_t B, int32_t T,
+cudaError_t launch_logits_backward(const void* logits, int32_t dtype, int64_t stride, const int64_t* seq_start,
+                                   int32_t V, int32_t B, int32_t T,
                                    const int32_t* lengths, const int32_t* tokens, const float* lse, const float* dlogp,
                                    const float* weight, void* grad, int32_t gdtype, int64_t gstride, int num_sms,
                                    cudaStream_t s) {
-  const BwArgs a{logits, stride, V, B, T, lengths, tokens, lse, dlogp, weight, grad, gstride};
+  const BwArgs a{logits, stride, seq_start, V, B, T, lengths, tokens, lse, dlogp, weight, grad, gstride};
   if (dtype == RLO_DTYPE_BF16)
     return gdtype == RLO_DTYPE_BF16 ? launch_bw<__nv_bfloat16, __nv_bfloat16>(a, num_sms, s)
                                     : launch_bw<__nv_bfloat16, float>(a, num_sms, s);

@@ -210,27 +210,27 @@ __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
   // Next loss-participating row of this cluster at or after `row` (the same
   // for every CTA of the cluster); rows passed over get their zero gradient
   // slice (streaming warps) and inactive outputs here.
+  // Gradient rows follow the actor logits' layout (padded or packed).
+  auto grad_row = [&](int64_t row) { return reinterpret_cast<GT*>(f.grad) + logits_row(a, 0, row) * f.gstride + c0; };
   auto next_active = [&](int64_t row) {
     for (; row < nrows; row += ncl) {
       if (row_active<true>(a, row, r == 0 && tid == 0)) break;
       if (r == 0 && tid == 0) write_inactive<true>(a, row);
-      if (!epi)
-        slice_grad<ET, GT>(nullptr, n, nullptr, reinterpret_cast<GT*>(f.grad) + row * f.gstride + c0, 0.f, 0.f, -1,
-                           0.f);
+      if (!epi && row_exists(a, row)) slice_grad<ET, GT>(nullptr, n, nullptr, grad_row(row), 0.f, 0.f, -1, 0.f);
     }
     return row;
   };
   auto backward = [&](int64_t row, int b) {
     const float* q = bc[b];
-    slice_grad<ET, GT>(reinterpret_cast<const ET*>(a.logits[0]) + row * a.stride[0] + c0, n, b ? smb1 : smb0,
-                       reinterpret_cast<GT*>(f.grad) + row * f.gstride + c0, q[0], q[1], __float_as_int(q[3]), q[2]);
+    slice_grad<ET, GT>(reinterpret_cast<const ET*>(a.logits[0]) + logits_off(a, 0, row) + c0, n, b ? smb1 : smb0,
+                       grad_row(row), q[0], q[1], __float_as_int(q[3]), q[2]);
   };
   int64_t prev = -1;
   int b = 0;
   for (int64_t row = next_active(blockIdx.x / K); row < nrows; row = next_active(row + ncl), b ^= 1) {
     if (!epi) {
       VV* sm = b ? smb1 : smb0;
-      const ET* rp0 = reinterpret_cast<const ET*>(a.logits[0]) + row * a.stride[0] + c0;
+      const ET* rp0 = reinterpret_cast<const ET*>(a.logits[0]) + logits_off(a, 0, row) + c0;
       Acc acc[NT];
 #pragma unroll
       for (int k = 0; k < NT; ++k) {
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
             slice_pass<ET, U, MATH | kMathGuard, false>(rp0, n, sm, acc[0]);
           }
         } else {
-          const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + row * a.stride[k] + c0;
+          const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + logits_off(a, k, row) + c0;
           stream_accumulate<kFT, ET, U, RLO_FUSED_PF != 0, false, MATH>(rp, n, true, acc[k]);
         }
       }

@@ -72,6 +72,7 @@ RLO_HOST_DEVICE inline int whiten_combine(const double* stats_all, int world, do
 struct VocabArgs {
   const void* logits[3];
   int64_t stride[3];
+  const int64_t* seq_start[3];  // packed layout per tensor (rlo_logits.seq_start), NULL = padded
   int32_t role[3];
   int32_t ntens;
   int32_t dtype;  // rlo_dtype shared by all tensors of the pass
@@ -149,7 +150,8 @@ cudaError_t launch_loss_weights(int32_t B, int32_t T, int32_t G, int32_t agg, do
 // batch -> out4[0..2] (fp64, exact integers); counts [B] scratch.
 cudaError_t launch_batch_counts(int32_t B, int32_t T, int32_t G, const int32_t* lengths, const uint8_t* mask,
                                 float* counts, double* out4, cudaStream_t s);
-cudaError_t launch_logits_backward(const void* logits, int32_t dtype, int64_t stride, int32_t V, int32_t B, int32_t T,
+cudaError_t launch_logits_backward(const void* logits, int32_t dtype, int64_t stride, const int64_t* seq_start,
+                                   int32_t V, int32_t B, int32_t T,
                                    const int32_t* lengths, const int32_t* tokens, const float* lse, const float* dlogp,
                                    const float* weight, void* grad, int32_t gdtype, int64_t gstride, int num_sms,
                                    cudaStream_t s);

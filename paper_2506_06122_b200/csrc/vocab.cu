@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
 #pragma unroll
     for (int k = 0; k < NT; ++k) {
       acc_init(acc[k]);
-      const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + row * a.stride[k];
+      const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + logits_off(a, k, row);
       if (k == 0 && ENT0) {
         if (RLO_ENT_GUARD_ALWAYS) {
           stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, vec_ok, acc[k]);

@@ -425,13 +425,32 @@ __device__ __forceinline__ void write_inactive(const VocabArgs& a, int64_t row) 
   }
 }
 
+// Row number of token `row` = (b, t) in logits tensor k: packed
+// (seq_start[b] + t) or padded (row itself).
+__device__ __forceinline__ int64_t logits_row(const VocabArgs& a, int k, int64_t row) {
+  const int64_t* ss = a.seq_start[k];
+  if (!ss) return row;
+  const int b = (int)(row / a.T);
+  return __ldg(ss + b) + (row - (int64_t)b * a.T);
+}
+__device__ __forceinline__ int64_t logits_off(const VocabArgs& a, int k, int64_t row) {
+  return logits_row(a, k, row) * a.stride[k];
+}
+// Does token `row` have a row in the actor logits (and the gradient)?  Packed
+// tensors hold only t < lengths[b]; padded ones hold every (b, t).
+__device__ __forceinline__ bool row_exists(const VocabArgs& a, int64_t row) {
+  if (!a.seq_start[0]) return true;
+  const int b = (int)(row / a.T);
+  return row - (int64_t)b * a.T < seq_len(a.lengths, b, a.T);
+}
+
 // Token gather for the row (one thread): bit-exact element loads.
 template <typename ET, int NT>
 __device__ __forceinline__ void gather_token(const VocabArgs& a, int64_t row, int& tok, bool& oov, float (&ztok)[NT]) {
   tok = __ldg(a.tokens + row);
   oov = tok < 0 || tok >= a.V;
 #pragma unroll
-  for (int k = 0; k < NT; ++k) ztok[k] = oov ? 0.f : load_logit<ET>(a.logits[k], row * a.stride[k] + tok);
+  for (int k = 0; k < NT; ++k) ztok[k] = oov ? 0.f : load_logit<ET>(a.logits[k], logits_off(a, k, row) + tok);
 }
 
 // Final cross-warp combine + outputs, executed by one full warp (all lanes):

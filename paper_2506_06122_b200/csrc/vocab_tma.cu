@@ -197,6 +197,7 @@ bool tma_eligible(const VocabArgs& a, int esz) {
   for (int k = 0; k < a.ntens; ++k) {
     if ((reinterpret_cast<uintptr_t>(a.logits[k]) & 15u) != 0) return false;
     if ((a.stride[k] * esz) % 16 != 0) return false;
+    if (a.seq_start[k]) return false;  // packed logits: the LDG kernel
   }
   return true;
 }

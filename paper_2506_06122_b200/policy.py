@@ -146,7 +146,10 @@ def _stream(stream, device):
     return C.c_void_p(s.cuda_stream)
 
 
-def _logits(t, name="logits"):
+def _logits(t, name="logits", seq_start=None):
+    """rlo_logits view of a [rows, V] (or [B, T, V]) CUDA tensor.  seq_start:
+    optional int64 CUDA tensor [B] (e.g. cu_seqlens[:-1]) for the packed /
+    varlen layout, token (b, t) = row seq_start[b] + t."""
     torch = _torch()
     if t is None:
         return None
@@ -166,6 +169,9 @@ def _logits(t, name="logits"):
     stride = t.stride(-2)
     L = _abi.rlo_logits()
     L.data, L.dtype, L.V, L.row_stride = t.data_ptr(), dt, t.shape[-1], stride
+    if seq_start is not None:
+        _check_dev(seq_start, torch.int64, f"{name} seq_start")
+        L.seq_start = seq_start.data_ptr()
     return L
 
 
@@ -225,7 +231,8 @@ class Objective:
         check(_abi.lib().rlo_sync(self._h, _stream(stream, self.device)))
 
     # -- the path -------------------------------------------------------------
-    def forward_logprobs(self, logits, tokens, lengths, entropy=False, token_logit=False, stream=None):
+    def forward_logprobs(self, logits, tokens, lengths, entropy=False, token_logit=False, seq_start=None,
+                         stream=None):
         """forward_logprobs (policy.cpp:210-233): log-prob of every valid
         response position.  logits [B,T,V] or [B*T,V]; tokens [B,T] int32;
         lengths [B] int32.  Returns dict of float32 [B,T] tensors."""
@@ -239,7 +246,8 @@ class Objective:
         if token_logit:
             out["token_logit"] = torch.empty_like(out["logp"])
         check(_abi.lib().rlo_forward_logprobs(
-            self._h, C.byref(_batch(lengths, tokens, None, T)), C.byref(_logits(logits)), _ptr(out["logp"]),
+            self._h, C.byref(_batch(lengths, tokens, None, T)), C.byref(_logits(logits, seq_start=seq_start)),
+            _ptr(out["logp"]),
             _ptr(out.get("entropy")), _ptr(out.get("token_logit")), _stream(stream, self.device)))
         return out
 
@@ -267,7 +275,7 @@ class Objective:
 
     def ppo_gradient(self, cfg: TrainConfig, tokens, lengths, actor_logits, advantages, mask=None, old_logits=None,
                      ref_logits=None, old_logprobs=None, ref_logprobs=None, seq_offset=0,
-                     outputs=("logp", "dlogp"), stream=None):
+                     outputs=("logp", "dlogp"), seq_start=None, stream=None):
         """ppo_gradient loss part (policy.cpp:313-374), fused over the logits.
         Accumulates per-sequence sums until merge_gradients().  Returns the
         requested per-token outputs ([B,T] float32): logp, old_logp, ref_logp,
@@ -283,10 +291,11 @@ class Objective:
         o = _abi.rlo_token_out()
         for k in ("logp", "old_logp", "ref_logp", "entropy", "dlogp", "loss", "lse"):
             setattr(o, k, res[k].data_ptr() if k in res else None)
-        L_old, L_ref = _logits(old_logits, "old_logits"), _logits(ref_logits, "ref_logits")
+        L_old = _logits(old_logits, "old_logits", seq_start)
+        L_ref = _logits(ref_logits, "ref_logits", seq_start)
         check(_abi.lib().rlo_ppo_gradient(
             self._h, C.byref(cfg.to_c()), C.byref(_batch(lengths, tokens, mask, T, seq_offset)),
-            C.byref(_logits(actor_logits, "actor_logits")), C.byref(L_old) if L_old else None,
+            C.byref(_logits(actor_logits, "actor_logits", seq_start)), C.byref(L_old) if L_old else None,
             C.byref(L_ref) if L_ref else None, _ptr(old_logprobs), _ptr(ref_logprobs), _ptr(advantages),
             C.byref(o), _stream(stream, self.device)))
         return res
@@ -323,7 +332,7 @@ class Objective:
 
     def ppo_gradient_fused(self, cfg: TrainConfig, tokens, lengths, actor_logits, advantages, weight, mask=None,
                            old_logits=None, ref_logits=None, old_logprobs=None, ref_logprobs=None, seq_offset=0,
-                           grad=None, grad_dtype=None, outputs=("logp", "dlogp"), stream=None):
+                           grad=None, grad_dtype=None, outputs=("logp", "dlogp"), seq_start=None, stream=None):
         """ppo_gradient + the actor backward epilogue in one read of the actor
         logits (policy.cpp:355-379).  Accumulates like ppo_gradient; returns
         (per-token outputs dict, grad [B*T, V])."""
@@ -343,16 +352,18 @@ class Objective:
         o = _abi.rlo_token_out()
         for k in ("logp", "old_logp", "ref_logp", "entropy", "dlogp", "loss", "lse"):
             setattr(o, k, res[k].data_ptr() if k in res else None)
-        L_old, L_ref = _logits(old_logits, "old_logits"), _logits(ref_logits, "ref_logits")
+        L_old = _logits(old_logits, "old_logits", seq_start)
+        L_ref = _logits(ref_logits, "ref_logits", seq_start)
         check(_abi.lib().rlo_ppo_gradient_fused(
             self._h, C.byref(cfg.to_c()), C.byref(_batch(lengths, tokens, mask, T, seq_offset)),
-            C.byref(_logits(actor_logits, "actor_logits")), C.byref(L_old) if L_old else None,
+            C.byref(_logits(actor_logits, "actor_logits", seq_start)), C.byref(L_old) if L_old else None,
             C.byref(L_ref) if L_ref else None, _ptr(old_logprobs), _ptr(ref_logprobs), _ptr(advantages),
             _ptr(weight), C.c_void_p(grad.data_ptr()), G.dtype, G.row_stride, C.byref(o),
             _stream(stream, self.device)))
         return res, grad
 
-    def logits_backward(self, tokens, lengths, logits, lse, dlogp, weight, grad=None, grad_dtype=None, stream=None):
+    def logits_backward(self, tokens, lengths, logits, lse, dlogp, weight, grad=None, grad_dtype=None, seq_start=None,
+                        stream=None):
         """Actor backward epilogue (policy.cpp:375-379): dL/dlogits rows
         w*dlogp*(onehot - softmax); returns the gradient tensor."""
         torch = _torch()
@@ -361,7 +372,8 @@ class Objective:
             grad = torch.empty(B * T, logits.shape[-1], dtype=grad_dtype or logits.dtype, device=logits.device)
         G = _logits(grad, "grad")
         check(_abi.lib().rlo_logits_backward(
-            self._h, C.byref(_batch(lengths, tokens, None, T)), C.byref(_logits(logits)), _ptr(lse), _ptr(dlogp),
+            self._h, C.byref(_batch(lengths, tokens, None, T)), C.byref(_logits(logits, seq_start=seq_start)), _ptr(lse),
+            _ptr(dlogp),
             _ptr(weight), C.c_void_p(grad.data_ptr()), G.dtype, G.row_stride, _stream(stream, self.device)))
         return grad
 

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     assert len(declared) >= 21
     for s in declared:
         assert hasattr(L, s), s
-    assert L.rlo_abi_version() == 1
+    assert L.rlo_abi_version() == _abi.ABI_VERSION  # include/rlo.h RLO_ABI_VERSION
 
 
 def test_library_is_sm100a_only():
@@ -149,3 +149,10 @@ def test_policy_worker_rejects_unknown_method():
         w = rlo.PolicyWorker.__new__(rlo.PolicyWorker)
         with pytest.raises(rlo.DispatchError, match="unimplemented method 'generate'"):
             rlo.PolicyWorker.call(w, "generate", rlo.Message())
+
+
+def test_binding_abi_version_matches_header():
+    import re
+    with open(_abi.HEADER) as f:
+        v = int(re.search(r"#define RLO_ABI_VERSION (\d+)", f.read()).group(1))
+    assert v == _abi.ABI_VERSION
