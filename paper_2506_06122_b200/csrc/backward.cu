@@ -123,10 +123,10 @@ struct In<__nv_bfloat16> {
 };
 
 template <typename ET, typename GT>
-__global__ void __launch_bounds__(kBwThreads) logits_backward_kernel(const BwArgs a, bool vec_ok) {
+__global__ void __launch_bounds__(kBwThreads) logits_backward_kernel(const BwArgs a) {
   constexpr int N = In<ET>::kN;
+  constexpr int kOutAlign = N * (int)sizeof(GT) < 16 ? N * (int)sizeof(GT) : 16;  // widest store used
   const int64_t nrows = (int64_t)a.B * a.T;
-  const int nvec = vec_ok ? a.V / N : 0;
   for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
     const int b = (int)(row / a.T), t = (int)(row - (int64_t)b * a.T);
     const bool valid = t < seq_len(a.lengths, b, a.T);
@@ -135,33 +135,45 @@ __global__ void __launch_bounds__(kBwThreads) logits_backward_kernel(const BwArg
     const int64_t lrow = a.seq_start ? __ldg(a.seq_start + b) + t : row;
     GT* g = reinterpret_cast<GT*>(a.grad) + lrow * a.gstride;
     const ET* z = reinterpret_cast<const ET*>(a.logits) + lrow * a.stride;
+    // A row not starting on a 16-byte boundary (e.g. V = 50257 contiguous)
+    // takes its first elements scalar; the body is vectorised when the
+    // gradient row is then aligned for the widest store too.
+    const int mis = (int)(reinterpret_cast<uintptr_t>(z) & 15u);
+    int head = min(a.V, mis ? (16 - mis) / (int)sizeof(ET) : 0);
+    if (reinterpret_cast<uintptr_t>(g + head) % kOutAlign) head = a.V;  // misaligned against each other: scalar row
+    const int nvec = (a.V - head) / N, tail0 = head + nvec * N;
+    const ET* zb = z + head;
+    GT* gb = g + head;
     if (scale == 0.f) {  // non-participating (or zero-gradient) row: zeros
       float zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int i = threadIdx.x; i < nvec; i += kBwThreads) Out<GT>::template store<N>(g + (int64_t)i * N, zero);
-      for (int v = nvec * N + threadIdx.x; v < a.V; v += kBwThreads) Out<GT>::one(g + v, 0.f);
+      for (int v = threadIdx.x; v < head; v += kBwThreads) Out<GT>::one(g + v, 0.f);
+      for (int i = threadIdx.x; i < nvec; i += kBwThreads) Out<GT>::template store<N>(gb + (int64_t)i * N, zero);
+      for (int v = tail0 + threadIdx.x; v < a.V; v += kBwThreads) Out<GT>::one(g + v, 0.f);
       continue;
     }
     const int tok = __ldg(a.tokens + row);
     const float nl = -__ldg(a.lse + row) * kL2E;
     const float ms = -scale;
+    auto one = [&](int v) {
+      float o = ms * ex2(fmaf(In<ET>::one(z + v), kL2E, nl));
+      if (v == tok) o += scale;
+      Out<GT>::one(g + v, o);
+    };
+    for (int v = threadIdx.x; v < head; v += kBwThreads) one(v);
     for (int i = threadIdx.x; i < nvec; i += kBwThreads) {
       float x[8], o[8];
-      In<ET>::load(z + (int64_t)i * N, x);
+      In<ET>::load(zb + (int64_t)i * N, x);
 #pragma unroll
       for (int k = 0; k < N; ++k) o[k] = ms * ex2(fmaf(x[k], kL2E, nl));  // -w*dlp*p_v
-      const int d = tok - i * N;
+      const int d = tok - head - i * N;
       if (d >= 0 && d < N) {
 #pragma unroll
         for (int k = 0; k < N; ++k)
           if (k == d) o[k] += scale;  // + w*dlp at the realised token
       }
-      Out<GT>::template store<N>(g + (int64_t)i * N, o);
+      Out<GT>::template store<N>(gb + (int64_t)i * N, o);
     }
-    for (int v = nvec * N + threadIdx.x; v < a.V; v += kBwThreads) {
-      float o = ms * ex2(fmaf(In<ET>::one(z + v), kL2E, nl));
-      if (v == tok) o += scale;
-      Out<GT>::one(g + v, o);
-    }
+    for (int v = tail0 + threadIdx.x; v < a.V; v += kBwThreads) one(v);
   }
 }
 
@@ -169,17 +181,12 @@ template <typename ET, typename GT>
 cudaError_t launch_bw(const BwArgs& a, int num_sms, cudaStream_t s) {
   const int64_t nrows = (int64_t)a.B * a.T;
   if (nrows == 0) return cudaSuccess;
-  constexpr int N = In<ET>::kN;
-  constexpr int64_t kOutAlign = N * sizeof(GT) < 16 ? N * sizeof(GT) : 16;  // widest store used
-  const bool vec_ok = (reinterpret_cast<uintptr_t>(a.logits) % 16 == 0) &&
-                      (reinterpret_cast<uintptr_t>(a.grad) % kOutAlign == 0) &&
-                      ((a.stride * (int64_t)sizeof(ET)) % 16 == 0) && ((a.gstride * (int64_t)sizeof(GT)) % kOutAlign == 0);
   auto kern = logits_backward_kernel<ET, GT>;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBwThreads, 0);
   int64_t grid = (int64_t)num_sms * (per_sm < 1 ? 1 : per_sm);
   if (grid > nrows) grid = nrows;
-  kern<<<(int)grid, kBwThreads, 0, s>>>(a, vec_ok);
+  kern<<<(int)grid, kBwThreads, 0, s>>>(a);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
           }
         } else {
           const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + logits_off(a, k, row) + c0;
-          stream_accumulate<kFT, ET, U, RLO_FUSED_PF != 0, false, MATH>(rp, n, true, acc[k]);
+          stream_accumulate<kFT, ET, U, RLO_FUSED_PF != 0, false, MATH>(rp, n, acc[k]);
         }
       }
 #pragma unroll

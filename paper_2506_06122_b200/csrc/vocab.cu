@@ -47,11 +47,6 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
   __shared__ float red[2][kWarps][NT][3];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t nrows = (int64_t)a.B * a.T;
-  bool vec_ok = true;
-#pragma unroll
-  for (int k = 0; k < NT; ++k)
-    vec_ok &= ((reinterpret_cast<uintptr_t>(a.logits[k]) & 15u) == 0) &&
-              (((a.stride[k] * (int64_t)sizeof(ET)) & 15) == 0);
   int buf = 0;
   for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
     if (!row_active<LOSS>(a, row, tid == 0)) {  // uniform across the CTA
@@ -69,18 +64,18 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
       const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + logits_off(a, k, row);
       if (k == 0 && ENT0) {
         if (RLO_ENT_GUARD_ALWAYS) {
-          stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, vec_ok, acc[k]);
+          stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, acc[k]);
         } else {
-          stream_accumulate<kThreads, ET, U, PF, true, MATH>(rp, a.V, vec_ok, acc[k]);
+          stream_accumulate<kThreads, ET, U, PF, true, MATH>(rp, a.V, acc[k]);
           if (!(isfinite(acc[k].s) && isfinite(acc[k].w))) {
             // -inf logits in this thread's share: redo it guarded (the share
             // was just streamed, so the re-read mostly hits L2)
             acc_init(acc[k]);
-            stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, vec_ok, acc[k]);
+            stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, acc[k]);
           }
         }
       } else
-        stream_accumulate<kThreads, ET, U, PF, false, MATH>(rp, a.V, vec_ok, acc[k]);
+        stream_accumulate<kThreads, ET, U, PF, false, MATH>(rp, a.V, acc[k]);
     }
 #pragma unroll
     for (int k = 0; k < NT; ++k) {

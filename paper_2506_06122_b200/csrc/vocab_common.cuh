@@ -234,16 +234,35 @@ __device__ __forceinline__ float load_logit(const void* base, int64_t off) {
   return Vec<ET>::scalar(reinterpret_cast<const ET*>(base) + off);
 }
 
+// One element, scalar (row heads / tails).
+template <typename ET, bool ENT>
+__device__ __forceinline__ void acc_scalar(const ET* p, Acc& a) {
+  const float z = Vec<ET>::scalar(p);
+  acc_rescale<ENT>(a, z);
+  float w = 0.f, s = 0.f;
+  acc_elem<ENT>(z, a.mL, s, w);
+  a.s += s;
+  if (ENT) a.w += w;
+}
+
 // One row (or row slice) of V elements streamed by NTH threads with U 128-bit
-// loads in flight per thread.  PF: software prefetch — the next batch's U loads are issued before the
-// current batch's math, doubling the bytes in flight per thread.
+// loads in flight per thread.  A row that does not start on a 16-byte
+// boundary (e.g. V = 50257 in a contiguous tensor) takes its first few
+// elements scalar and the aligned body vectorised.  PF: software prefetch —
+// the next batch's U loads are issued before the current batch's math,
+// doubling the bytes in flight per thread.
 template <int NTH, typename ET, int U, bool PF, bool ENT, int MATH>
-__device__ __forceinline__ void stream_accumulate(const ET* __restrict__ row, int V, bool vec_ok, Acc& a) {
+__device__ __forceinline__ void stream_accumulate(const ET* __restrict__ row, int V, Acc& a) {
   using VT = Vec<ET>;
   using VV = typename VT::V;
   constexpr int kStep = NTH * U;
   const int tid = threadIdx.x;
-  const int nvec = vec_ok ? V / VT::kElems : 0;
+  const int mis = (int)(reinterpret_cast<uintptr_t>(row) & 15u);
+  const int head = min(V, mis ? (16 - mis) / (int)sizeof(ET) : 0);  // elements before the first 16-byte boundary
+  if (tid < head) acc_scalar<ET, ENT>(row + tid, a);
+  row += head;
+  V -= head;
+  const int nvec = V / VT::kElems;
   const int nfull = nvec / kStep * kStep;
   const VV* __restrict__ vrow = reinterpret_cast<const VV*>(row) + tid;
   if (PF) {
@@ -278,15 +297,7 @@ __device__ __forceinline__ void stream_accumulate(const ET* __restrict__ row, in
     }
     VT::template accumulate<U, ENT, MATH>(v, a);
   }
-  // scalar tail (or the whole row when rows are not 16-byte aligned)
-  for (int i = nvec * VT::kElems + tid; i < V; i += NTH) {
-    const float z = VT::scalar(row + i);
-    acc_rescale<ENT>(a, z);
-    float w = 0.f, s = 0.f;
-    acc_elem<ENT>(z, a.mL, s, w);
-    a.s += s;
-    if (ENT) a.w += w;
-  }
+  for (int i = nvec * VT::kElems + tid; i < V; i += NTH) acc_scalar<ET, ENT>(row + i, a);  // scalar tail
 }
 
 struct RowResult {

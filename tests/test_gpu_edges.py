@@ -123,3 +123,32 @@ def test_all_masked_batch_raises_reference_error(env):
     with pytest.raises(rlo.TrainingError) as e:
         obj.merge_gradients(cfg)
     assert str(e.value) == "merge_gradients: batch contains no loss-participating tokens"
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_unaligned_rows_head_body_tail(env, dt):
+    """V = 50257 in a contiguous tensor: every row starts at a different
+    offset from a 16-byte boundary (scalar head, vector body, scalar tail)."""
+    torch, rlo, obj = env
+    rng = np.random.default_rng(7)
+    B, T, V = 3, 11, 50257
+    tdt = torch.float32 if dt == "f32" else torch.bfloat16
+    x = (torch.randn(B * T, V, generator=torch.Generator().manual_seed(3)) * 3).to(tdt).cuda()
+    toks = rng.integers(0, V, (B, T)).astype(np.int32)
+    toks[0, :8] = np.arange(8)  # tokens inside the scalar head
+    out = obj.forward_logprobs(x, dev(torch, toks), dev(torch, np.full(B, T, np.int32)), entropy=True)
+    lp, ent = out["logp"].cpu().numpy().ravel(), out["entropy"].cpu().numpy().ravel()
+    rows = x.float().cpu().numpy().astype(np.float64)
+    for i in range(B * T):
+        lse, h = O.logsoftmax_row(rows[i])
+        assert close(lp[i], rows[i, toks.ravel()[i]] - lse), i
+        assert abs(ent[i] - h) <= 2e-5 * max(1.0, h), i
+    # backward epilogue on the same unaligned rows (fp32 gradient) vs the oracle
+    w = torch.full((B, T), 0.5, device="cuda")
+    dl = torch.full((B, T), -1.25, device="cuda")
+    lse = torch.from_numpy(np.array([O.logsoftmax_row(r)[0] for r in rows], np.float32).reshape(B, T)).cuda()
+    g = obj.logits_backward(dev(torch, toks), dev(torch, np.full(B, T, np.int32)), x, lse, dl, w,
+                            grad_dtype=torch.float32).cpu().numpy()
+    for i in (0, 1, 17, B * T - 1):
+        want = O.logits_backward_row(rows[i], int(toks.ravel()[i]), 0.5 * -1.25)
+        assert np.abs(g[i] - want).max() <= 1e-5 * 0.625 + 1e-12, i
