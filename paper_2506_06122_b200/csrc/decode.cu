@@ -54,28 +54,28 @@ __device__ __forceinline__ float logit<__nv_bfloat16>(const __nv_bfloat16* p, in
 }
 
 // exp(t) for t <= 0 in fp64 (the reference's std::exp precision, <= 1 ulp):
-// t = (64k + j) ln2/64 + r, |r| <= ln2/128; exp(t) = 2^k * 2^(j/64) * e^r with
-// 2^(j/64) from a 64-entry shared table and e^r from a degree-5 Taylor
-// polynomial (truncation r^6/720 < 4e-17).  10 fp64 operations instead of the
+// t = (256k + j) ln2/256 + r, |r| <= ln2/512; exp(t) = 2^k * 2^(j/256) * e^r
+// with 2^(j/256) from a 256-entry shared table and e^r from a degree-4 Taylor
+// polynomial (truncation r^5/120 < 4e-17).  9 fp64 operations instead of the
 // ~20 of the library exp(); t < -708 is clamped (3e-308, below every sum it
 // enters).
+constexpr int kExpTab = 256;
 __device__ __forceinline__ double exp_neg(double t, const double* __restrict__ tab) {
   t = fmax(t, -708.0);  // branch-free: exp(-708) = 3e-308 stands in for 0 (and for -inf logits)
-  constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round to integer
-  constexpr double k64Ln2 = 92.332482616893656;  // 64 / ln 2
-  constexpr double kLn2o64Hi = 0x1.62e42fefa0000p-7, kLn2o64Lo = 0x1.cf79abc9e3b3ap-46;
-  const double s = fma(t, k64Ln2, kMagic);
+  constexpr double kMagic = 6755399441055744.0;   // 1.5 * 2^52: round to integer
+  constexpr double k256Ln2 = 369.32993046757462;  // 256 / ln 2
+  constexpr double kLn2o256Hi = 0x1.62e42fefa0000p-9, kLn2o256Lo = 0x1.cf79abc9e3b3ap-48;
+  const double s = fma(t, k256Ln2, kMagic);
   const int n = __double2loint(s);
   const double nf = s - kMagic;
-  double r = fma(nf, -kLn2o64Hi, t);
-  r = fma(nf, -kLn2o64Lo, r);
-  double p = fma(r, 1.0 / 120, 1.0 / 24);
-  p = fma(p, r, 1.0 / 6);
+  double r = fma(nf, -kLn2o256Hi, t);
+  r = fma(nf, -kLn2o256Lo, r);
+  double p = fma(r, 1.0 / 24, 1.0 / 6);
   p = fma(p, r, 0.5);
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
-  const double v = tab[n & 63] * p;
-  return __longlong_as_double(__double_as_longlong(v) + ((long long)(n >> 6) << 52));
+  const double v = tab[n & (kExpTab - 1)] * p;
+  return __longlong_as_double(__double_as_longlong(v) + ((long long)(n >> 8) << 52));
 }
 
 template <typename ET>
@@ -132,14 +132,14 @@ __global__ void __launch_bounds__(kDecWarps * 32)
                   uint64_t version, const uint64_t* __restrict__ keys, const uint64_t* __restrict__ positions,
                   int32_t* __restrict__ out_tok, float* __restrict__ out_lp) {
   constexpr int E = DVec<ET>::E;
-  __shared__ double tab[64];
+  __shared__ double tab[kExpTab];
   __shared__ double s_t[kDecWarps];
   __shared__ float s_m[kDecWarps], s_ml[kDecWarps], s_su[kDecWarps];
   __shared__ double s_base, s_thresh, s_lse;
   __shared__ float s_M;
   __shared__ int s_warp, s_pick;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x < 64) tab[threadIdx.x] = exp2((double)threadIdx.x / 64.0);
+  for (int j = threadIdx.x; j < kExpTab; j += blockDim.x) tab[j] = exp2((double)j / kExpTab);
   __syncthreads();
   const double inv_t = 1.0 / temp;
   const bool unit_t = temp == 1.0;
