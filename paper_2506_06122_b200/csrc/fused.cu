@@ -352,7 +352,7 @@ int env_int(const char* name, int dflt) {
 template <typename ET, typename GT, int NT>
 cudaError_t launch_t(const FusedArgs& f, int K, cudaStream_t s) {
   constexpr int U = sizeof(ET) == 4 ? 8 : 4;
-  constexpr int MATH = sizeof(ET) == 4 ? 1 : 4;  // the vocab pass's measured defaults
+  constexpr int MATH = sizeof(ET) == 4 ? 1 : 6;  // the vocab pass's measured defaults
   auto kern = fused_kernel<ET, GT, NT, U, MATH>;
   const size_t smem = (size_t)f.slice * sizeof(ET) * 2;  // double-buffered actor slice
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

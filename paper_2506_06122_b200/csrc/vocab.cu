@@ -147,11 +147,11 @@ cudaError_t launch_impl(const VocabArgs& a, int num_sms, cudaStream_t s) {
   return launch_ldg_layout<ET, NT, LOSS, ENT0, MATH>(a, num_sms, s);
 }
 
-// Instruction mix (vocab_common.cuh): fp32 {0, 1}, default 1; bf16 {1..5}, default 4 (profiles/r1_vocab_sweep.txt).
+// Instruction mix (vocab_common.cuh): fp32 {0, 1}, default 1; bf16 {1..6}, default 6 (profiles/r1_vocab_sweep.txt).
 template <typename ET, int NT, bool LOSS, bool ENT0>
 cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
   if ((int64_t)a.B * a.T == 0) return cudaSuccess;
-  const int math = env_int("RLO_VOCAB_MATH", sizeof(ET) == 2 ? 4 : 1);
+  const int math = env_int("RLO_VOCAB_MATH", sizeof(ET) == 2 ? 6 : 1);
   if constexpr (sizeof(ET) == 4) {
     return math == 0 ? launch_impl<ET, NT, LOSS, ENT0, 0>(a, num_sms, s)
                      : launch_impl<ET, NT, LOSS, ENT0, 1>(a, num_sms, s);
@@ -161,6 +161,7 @@ cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
       case 3: return launch_impl<ET, NT, LOSS, ENT0, 3>(a, num_sms, s);
       case 4: return launch_impl<ET, NT, LOSS, ENT0, 4>(a, num_sms, s);
       case 5: return launch_impl<ET, NT, LOSS, ENT0, 5>(a, num_sms, s);
+      case 6: return launch_impl<ET, NT, LOSS, ENT0, 6>(a, num_sms, s);
       default: return launch_impl<ET, NT, LOSS, ENT0, 2>(a, num_sms, s);
     }
   }

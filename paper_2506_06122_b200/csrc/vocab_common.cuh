@@ -87,13 +87,16 @@ __device__ __forceinline__ void acc_warp_reduce(Acc& a) {
 //   3  as 2 with 2 of 4 pairs (50% offload);
 //   4  degree-4 polynomial on 1 of 4 pairs of every row, the entropy
 //      (actor) row included (25% of all exponentials);
-//   5  degree-4 polynomial on 2 of 4 pairs of the old/ref rows (50%).
+//   5  degree-4 polynomial on 2 of 4 pairs of the old/ref rows (50%);
+//   6  as 4 on the old/ref rows, the entropy (actor) row all MUFU.
 // Degree 4 has relative error 2.9e-6 per term, so with at most half of a
 // row's mass offloaded the lse error stays below 1.5e-6.
 
 // MATH -> polynomial degree of the offloaded pairs (0: none) and whether half
 // (rather than a quarter) of the old/ref element pairs are offloaded.
-__host__ __device__ constexpr int poly_deg(int math) { return math == 2 || math == 3 ? 5 : math == 4 || math == 5 ? 4 : 0; }
+__host__ __device__ constexpr int poly_deg(int math) {
+  return math == 2 || math == 3 ? 5 : math == 4 || math == 5 || math == 6 ? 4 : 0;
+}
 __host__ __device__ constexpr bool poly_half(int math) { return math == 3 || math == 5; }
 __host__ __device__ constexpr int poly_deg_ent(int math) { return math == 4 ? 4 : 0; }
 // Template MATH values may carry kMathGuard (the guarded entropy-row variant).

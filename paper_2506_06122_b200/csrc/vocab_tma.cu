@@ -229,7 +229,8 @@ cudaError_t launch_tma(const VocabArgs& a, int num_sms, cudaStream_t s) {
   RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 2)     \
   RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 3)     \
   RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 4)     \
-  RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 5)
+  RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 5)     \
+  RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 6)
 RLO_INST_F(1, false, false)
 RLO_INST_F(1, false, true)
 RLO_INST_F(1, true, true)
