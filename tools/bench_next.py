@@ -41,14 +41,17 @@ def timed(fn, iters=5, warm=2):
 
 
 def bench_decode(obj):
-    for rows, V, dt in ((4096, 152064, torch.bfloat16), (32768, 152064, torch.bfloat16), (32768, 32000, torch.float32)):
-        x = torch.empty(rows, V, dtype=dt, device="cuda")
+    for rows, V, dt, stride in ((4096, 152064, torch.bfloat16, 152064), (32768, 152064, torch.bfloat16, 152064),
+                                (32768, 32000, torch.float32, 32000), (32768, 50257, torch.bfloat16, 50257),
+                                (32768, 50257, torch.bfloat16, 50264)):
+        x = torch.empty(rows, stride, dtype=dt, device="cuda")[:, :V]
         rlo.synth_logits(x, seed=1, model=0)
         keys = torch.arange(rows, dtype=torch.int64, device="cuda") * 7919
         pos = torch.full((rows,), 17, dtype=torch.int64, device="cuda")
         ms = timed(lambda: obj.decode_sample(x, 0.8, 42, 3, keys, pos))
         byts = rows * V * x.element_size()
-        print(json.dumps({"row": "decode", "rows": rows, "V": V, "dtype": str(dt).split(".")[-1], "ms": ms,
+        print(json.dumps({"row": "decode", "rows": rows, "V": V, "stride": stride, "dtype": str(dt).split(".")[-1],
+                          "ms": ms,
                           "rows_per_s": rows / ms * 1e3, "gbs_one_pass": byts / ms / 1e6,
                           "note": "fp64 tempered CDF walk; bytes = one pass over each row"}), flush=True)
         del x
