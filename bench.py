@@ -46,9 +46,10 @@ CONFIGS = {
     4: dict(name="cfg4: long-CoT RLVR 32 prompts x 8 responses x 16384 tokens, V=152064 bf16, dual-clip c=3, "
                  "global whitening", B=256, T=16384, V=152064, dtype="bf16", est="grpo", G=8, whiten=True,
             kl_est="k3", kl_coef=0.001, dual=3.0, agg="token-mean", mb_seqs=2),
-    5: dict(name="cfg5: GRPO 1024 prompts x 8 responses x 4096 tokens, V=152064 bf16, global whitening",
+    5: dict(name="cfg5: GRPO 1024 prompts x 8 responses x 4096 tokens, V=152064 bf16, global whitening, "
+                 "global batch sharded over the GPUs",
             B=8192, T=4096, V=152064, dtype="bf16", est="grpo", G=8, whiten=True, kl_est="k3", kl_coef=0.001,
-            dual=0.0, agg="token-mean", mb_seqs=8),
+            dual=0.0, agg="token-mean", mb_seqs=8, global_batch=True),
 }
 
 
@@ -127,8 +128,12 @@ def make_cfg(rlo, c):
 
 
 def side_inputs(c, rank, seed):
-    """Per-rank synthetic SampleBatch side arrays (host numpy)."""
+    """Per-rank synthetic SampleBatch side arrays (host numpy).  Global-batch
+    configs draw the whole batch from one seed and keep this rank's shard."""
     B, T = c["B"], c["T"]
+    if c.get("global_batch"):
+        full = side_inputs(dict(c, B=c["B_global"], global_batch=False), 0, seed)
+        return {k: v[c["b0"]:c["b0"] + B] for k, v in full.items()}
     rng = np.random.default_rng(seed * 1000 + rank)
     lengths = np.full(B, T, np.int32)  # throughput runs: full-length responses
     if c["est"] == "grpo":
@@ -162,13 +167,18 @@ def run_ours(args, c):
         dist.broadcast_object_list(uid, src=0)
         obj.init_comm(uid[0], rank, world)
 
+    if c.get("global_batch"):
+        # batch-sharded (BASELINE cfg 5): the global batch is split on group
+        # boundaries (rlo_shard_plan, the reference's split rule over groups)
+        b0, nb = rlo.shard_plan(c["B"], c["G"], world, rank)
+        c = dict(c, B_global=c["B"], B=nb, b0=b0)
     B, T, V = c["B"], c["T"], c["V"]
     tdt = torch.float32 if c["dtype"] == "f32" else torch.bfloat16
     esz = 4 if c["dtype"] == "f32" else 2
     mb = c["mb_seqs"] or B
     key_rows = mb * T
     seed = args.seed
-    row_off = rank * B * T
+    row_off = (c["b0"] if c.get("global_batch") else rank * B) * T
     stream = torch.cuda.current_stream(dev)
 
     # resident logits: all rows, or one micro-batch chunk reused by every micro-batch
@@ -244,15 +254,17 @@ def run_ours(args, c):
     per_row_side = 4 + 4 + 17  # token id, advantage, per-token results written for the reduction
     bytes_per_launch = mb * T * (3 * V * esz + per_row_side)
     achieved = bytes_per_launch / (vocab_avg_ms * 1e-3) / 1e9
-    value = world * tokens_per_step * args.steps / (ms * 1e-3)
+    job_tokens = c.get("B_global", world * B) * T  # all ranks' scored tokens per step
+    value = job_tokens * args.steps / (ms * 1e-3)
 
     out = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if c.get("global_batch") else "weak",
         "vs_baseline": None, "dtype": c["dtype"],
         "data": "synthetic: counter-hash logits (include/rlo_synth.h), random-init side arrays",
         "config": {"workload": c["name"], "B_per_rank": B, "T": T, "V": V, "logits_tensors": 3,
-                   "global_batch_seqs": B * world, "micro_batch_seqs": mb,
+                   "global_batch_seqs": c.get("B_global", B * world), "micro_batch_seqs": mb,
                    "resident_logit_rows": key_rows,
                    "l2": f"inputs larger than L2: {3 * key_rows * V * esz / 1e9:.1f} GB of logits streamed per "
                          f"micro-batch vs 126 MB L2",
@@ -341,10 +353,11 @@ def run_p1(args, c, obj, rlo, torch, cfg, logits, tokens, dside, adv, logp, stre
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     world = dist.get_world_size() if dist else 1
+    job_tokens = c.get("B_global", world * B) * T
     vk = float(np.mean([a.elapsed_time(b) for a, b in ev]))
     bytes_per_launch = mb * T * (V * esz + 4 + 4 + 8 + 17)
     peak, _ = load_peaks()
-    return {"value": world * B * T * steps / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms / steps,
+    return {"value": job_tokens * steps / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms / steps,
             "logits_tensors": 1, "achieved_gbs": bytes_per_launch / (vk * 1e-3) / 1e9,
             "frac": bytes_per_launch / (vk * 1e-3) / 1e9 / peak, "avg_launch_ms": vk,
             "loss": st.loss, "note": "actor logits only; old/ref log-probs precomputed (untimed)"}
@@ -359,7 +372,7 @@ def run_e2e(args, c, obj, rlo, torch, cfg, logits, side, dev, stream, dist, key_
     pin = {k: torch.from_numpy(v).pin_memory() for k, v in side.items()}
     tok_host = torch.empty(B, T, dtype=torch.int32).pin_memory()
     rlo.synth_tokens(tok_host_dev := torch.empty(B, T, dtype=torch.int32, device=dev), V, seed=args.seed,
-                     row_key_offset=int(os.environ.get("RANK", "0")) * B * T, key_rows=key_rows)
+                     row_key_offset=c.get("b0", int(os.environ.get("RANK", "0")) * B) * T, key_rows=key_rows)
     tok_host.copy_(tok_host_dev)
     adv_host = torch.empty(B, T, dtype=torch.float32).pin_memory()
     logp_host = torch.empty(B, T, dtype=torch.float32).pin_memory()
@@ -409,7 +422,7 @@ def run_e2e(args, c, obj, rlo, torch, cfg, logits, side, dev, stream, dist, key_
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         el = float(tt.item())
     world = dist.get_world_size() if dist else 1
-    return {"value": world * B * T * args.steps / el, "unit": "tokens/s", "h2d_bytes_per_step": hb_in,
+    return {"value": c.get("B_global", world * B) * T * args.steps / el, "unit": "tokens/s", "h2d_bytes_per_step": hb_in,
             "d2h_bytes_per_step": hb_out + 64, "api": api, "ms_per_step": 1e3 * el / args.steps}
 
 
