@@ -166,7 +166,7 @@ def _logits(t, name="logits", seq_start=None):
         raise InputError(f"{name}: vocab dimension must be contiguous")
     if t.dim() == 3 and t.stride(0) != t.shape[1] * t.stride(1):
         raise InputError(f"{name}: rows must be uniformly strided")
-    stride = t.stride(-2)
+    stride = t.stride(-2) if t.dim() >= 2 and t.shape[-2] > 1 else t.shape[-1]  # a single row's stride is moot
     L = _abi.rlo_logits()
     L.data, L.dtype, L.V, L.row_stride = t.data_ptr(), dt, t.shape[-1], stride
     if seq_start is not None:

@@ -229,6 +229,44 @@ def config_cases():
     return out, splits
 
 
+def extension_cases(rng):
+    """Pin the extensions the reference lacks to its own code where an identity
+    exists: GAE with lambda = 1 telescopes to the reference's discounted
+    return minus the value; GRPO on one group of one-token samples with
+    eps = 1e-8 is the reference's whitening; the entropy of a row is
+    -sum p log p over the reference's own full log-softmax."""
+    gae, grpo, ent = [], [], []
+    for k in range(4):
+        B, T = int(rng.integers(2, 7)), int(rng.integers(3, 20))
+        lengths = rng.integers(0, T + 1, B)
+        lengths[0] = T
+        mask = (rng.random(B * T) < 0.7).astype(np.uint8)
+        g = float(rng.choice([1.0, 0.9, 0.99]))
+        rt = rng.standard_normal(B * T) * 2.0
+        vals = rng.standard_normal(B * T) * 0.5
+        kw = dict(gamma=g, reward_clip=1e6, advantage_clip=1e9)
+        ref = O.ref_compute_advantages(O.TrainConfig(**kw), B, T, lengths, mask, rewards_tok=rt)
+        valid = (np.arange(T)[None, :] < lengths[:, None]).ravel()
+        expect = np.where(valid, ref - vals, 0.0)
+        gae.append(dict(cfg=dict(kw, adv_estimator=2, lambd=1.0), B=B, T=T, lengths=lengths.tolist(),
+                        mask=mask.tolist(), rewards_tok=rt.tolist(), values=vals.tolist(), expect=expect.tolist()))
+    for B in (4, 8, 16):
+        rs = rng.standard_normal(B) * 2.0
+        kw = dict(advantage_clip=10.0, reward_clip=20.0)
+        ref = O.ref_compute_advantages(O.TrainConfig(whiten_advantages=1, **kw), B, 1, [1] * B, None, rewards_seq=rs)
+        grpo.append(dict(cfg=dict(kw, adv_estimator=1, group_size=B, grpo_eps=1e-8), B=B, T=1, lengths=[1] * B,
+                         rewards_seq=rs.tolist(), expect=ref.tolist()))
+    for V, scale in [(9, 1.0), (57, 3.0), (1000, 3.0), (4099, 8.0), (8192, 3.0)]:
+        z = (rng.standard_normal(V) * scale).astype(np.float32)
+        _, full = O.ref_logsoftmax_rows(z.astype(np.float64), [0], full=True)
+        lp = full[0]
+        ent.append(dict(V=V, row=z.tolist(), entropy=float(-(np.exp(lp) * lp).sum())))
+    with open(os.path.join(HERE, "extensions.json"), "w") as f:
+        json.dump({"source": "identities onto compute_advantages policy.cpp:257-311 (GAE lambda=1, GRPO one group "
+                             "of T=1 samples = whitening) and the full log-softmax policy.cpp:116-122 (entropy)",
+                   "gae_lambda1": gae, "grpo_one_group": grpo, "entropy": ent}, f)
+
+
 def main():
     O.build(with_ref=True)
     rng = np.random.default_rng(20250606)
@@ -238,6 +276,7 @@ def main():
     ppo_cases(rng)
     value_cases(np.random.default_rng(474))
     decode_cases(np.random.default_rng(143))
+    extension_cases(np.random.default_rng(2506))
     extra.update(jsonl_cases())
     cfgs, splits = config_cases()
     with open(os.path.join(HERE, "misc.json"), "w") as f:

@@ -463,3 +463,35 @@ def test_full_size_config2_properties(env):
     assert abs(st1.mean_ratio - 1.0) <= 1e-7 and close(st1.loss, -float(adv.double().mean()), 1e-6)
     del L
     torch.cuda.empty_cache()
+
+
+def test_extensions_pinned_to_reference_identities(env):
+    """GAE (lambda = 1) = the reference's discounted return minus the value;
+    GRPO on one group of one-token samples = the reference's whitening; the
+    entropy = -sum p log p of the reference's full log-softmax
+    (tests/golden/extensions.json, made by the reference's own code)."""
+    torch, rlo, obj = env
+    ext = golden("extensions.json")
+    for c in ext["gae_lambda1"]:
+        B, T = c["B"], c["T"]
+        cfg = rlo.TrainConfig(**{k: v for k, v in c["cfg"].items()})
+        adv = obj.compute_advantages(cfg, dev(torch, np.asarray(c["lengths"], np.int32)), T=T,
+                                     mask=dev(torch, np.asarray(c["mask"], np.uint8).reshape(B, T)),
+                                     rewards=dev(torch, np.asarray(c["rewards_tok"], np.float32).reshape(B, T)),
+                                     values=dev(torch, np.asarray(c["values"], np.float32).reshape(B, T)))
+        assert_close(adv.cpu().numpy().ravel(), c["expect"], tol=2e-5, what="gae lambda=1")
+    for c in ext["grpo_one_group"]:
+        cfg = rlo.TrainConfig(**c["cfg"])
+        adv = obj.compute_advantages(cfg, dev(torch, np.asarray(c["lengths"], np.int32)), T=c["T"],
+                                     scalar_rewards=dev(torch, np.asarray(c["rewards_seq"], np.float32)))
+        # fp32 rewards on the device: compare with the identity on the same fp32-rounded inputs
+        rs = np.asarray(c["rewards_seq"], np.float32).astype(np.float64)
+        want = np.clip((rs - rs.mean()) / (rs.std() + 1e-8), -10.0, 10.0)
+        assert_close(adv.cpu().numpy().ravel(), want, tol=2e-5, what="grpo one group")
+        assert_close(want, c["expect"], tol=1e-5, what="identity vs reference")
+    for c in ext["entropy"]:
+        row = np.asarray(c["row"], np.float32)
+        out = obj.forward_logprobs(dev(torch, row[None, :]), dev(torch, np.zeros((1, 1), np.int32)),
+                                   dev(torch, np.array([1], np.int32)), entropy=True)
+        h = float(out["entropy"].item())
+        assert abs(h - c["entropy"]) <= 1e-5 * max(1.0, abs(c["entropy"])), (c["V"], h, c["entropy"])

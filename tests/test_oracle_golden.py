@@ -222,3 +222,33 @@ def test_grpo_and_gae_definitions():
     delta = r + 0.99 * vn - v
     brute = [sum((0.99 * 0.95) ** (u - t) * delta[u] for u in range(t, T)) for t in range(T)]
     assert np.max(np.abs(adv - brute)) < 1e-12 and np.max(np.abs(ret - (adv + v))) < 1e-12
+
+
+def _ext():
+    with open(os.path.join(G, "extensions.json")) as f:
+        return json.load(f)
+
+
+def test_gae_lambda1_is_reference_return_minus_value():
+    """GAE (an extension) pinned to the reference: lambda = 1 telescopes to the
+    reference's discounted return minus the critic value."""
+    for c in _ext()["gae_lambda1"]:
+        adv, _ = O.compute_advantages(O.TrainConfig(**c["cfg"]), c["B"], c["T"], c["lengths"], c["mask"],
+                                      rewards_tok=c["rewards_tok"], values=c["values"])
+        np.testing.assert_allclose(adv, c["expect"], rtol=1e-9, atol=1e-9)
+
+
+def test_grpo_one_group_is_reference_whitening():
+    """GRPO (an extension) pinned to the reference: one group of one-token
+    samples with eps = 1e-8 is the reference's whitening of the rewards."""
+    for c in _ext()["grpo_one_group"]:
+        adv, _ = O.compute_advantages(O.TrainConfig(**c["cfg"]), c["B"], c["T"], c["lengths"],
+                                      rewards_seq=c["rewards_seq"])
+        np.testing.assert_allclose(adv, c["expect"], rtol=1e-9, atol=1e-12)
+
+
+def test_entropy_is_reference_softmax_entropy():
+    """Entropy (an extension) pinned to the reference's own full log-softmax."""
+    for c in _ext()["entropy"]:
+        _, h = O.logsoftmax_row(np.asarray(c["row"], np.float64))
+        assert abs(h - c["entropy"]) <= 1e-11 * max(1.0, abs(c["entropy"])), c["V"]
