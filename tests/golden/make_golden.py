@@ -261,10 +261,30 @@ def extension_cases(rng):
         _, full = O.ref_logsoftmax_rows(z.astype(np.float64), [0], full=True)
         lp = full[0]
         ent.append(dict(V=V, row=z.tolist(), entropy=float(-(np.exp(lp) * lp).sum())))
+    # aggregation / dual-clip identities: with equal lengths and no mask every
+    # sequence and group holds the same token count, so seq-mean-token-mean and
+    # group-mean equal the reference's token-mean; a dual-clip cap that never
+    # binds (c = 1e9) leaves the reference's clipped surrogate unchanged
+    agg = []
+    for k in range(4):
+        V, G = int(rng.choice([17, 64])), int(rng.choice([2, 3]))
+        B, T = G * int(rng.integers(1, 4)), int(rng.integers(2, 9))
+        row = rng.standard_normal(V) * 1.5
+        lengths = np.full(B, T)
+        tokens = rng.integers(0, V, B * T).astype(np.int32)
+        full = O.ref_logsoftmax_rows(row, [0], full=True)[1][0]
+        lp = full[tokens]
+        old = lp + rng.uniform(-0.4, 0.4, B * T)
+        ref_lp = lp + rng.uniform(-0.3, 0.3, B * T)
+        adv = rng.uniform(-1, 1, B * T)
+        kw = dict(clip_eps=0.2, kl_coef=float(rng.choice([0.0, 0.1])))
+        st = O.ref_ppo_stats_b2(row, B, T, lengths, tokens, None, old, ref_lp, adv, O.TrainConfig(**kw), 1)
+        agg.append(dict(cfg=kw, G=G, V=V, B=B, T=T, row=row.tolist(), lengths=lengths.tolist(), tokens=tokens.tolist(),
+                        old=old.tolist(), ref=ref_lp.tolist(), adv=adv.tolist(), ref_stats=st))
     with open(os.path.join(HERE, "extensions.json"), "w") as f:
         json.dump({"source": "identities onto compute_advantages policy.cpp:257-311 (GAE lambda=1, GRPO one group "
                              "of T=1 samples = whitening) and the full log-softmax policy.cpp:116-122 (entropy)",
-                   "gae_lambda1": gae, "grpo_one_group": grpo, "entropy": ent}, f)
+                   "gae_lambda1": gae, "grpo_one_group": grpo, "entropy": ent, "aggregation": agg}, f)
 
 
 def main():

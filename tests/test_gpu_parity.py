@@ -495,3 +495,21 @@ def test_extensions_pinned_to_reference_identities(env):
                                    dev(torch, np.array([1], np.int32)), entropy=True)
         h = float(out["entropy"].item())
         assert abs(h - c["entropy"]) <= 1e-5 * max(1.0, abs(c["entropy"])), (c["V"], h, c["entropy"])
+
+
+def test_aggregation_and_dual_clip_identities_on_gpu(env):
+    """GPU seq-mean-token-mean / group-mean / never-binding dual-clip on
+    equal-length unmasked batches reproduce the reference's token-mean loss."""
+    torch, rlo, obj = env
+    for c in golden("extensions.json")["aggregation"]:
+        B, T = c["B"], c["T"]
+        row = np.asarray(c["row"], np.float32)
+        logits = dev(torch, np.tile(row, (B * T, 1)))
+        for extra in (dict(loss_agg=1), dict(loss_agg=3, group_size=c["G"]), dict(dual_clip_c=1e9)):
+            cfg = rlo.TrainConfig(**c["cfg"], **extra)
+            obj.ppo_gradient(cfg, dev(torch, _arr(c["tokens"], np.int32).reshape(B, T)),
+                             dev(torch, _arr(c["lengths"], np.int32)), logits, dev(torch, _arr(c["adv"]).reshape(B, T)),
+                             old_logprobs=dev(torch, _arr(c["old"]).reshape(B, T)),
+                             ref_logprobs=dev(torch, _arr(c["ref"]).reshape(B, T)))
+            st = obj.merge_gradients(cfg)
+            assert close(st.loss, c["ref_stats"]["loss"], tol=2e-5), (extra, st.loss, c["ref_stats"]["loss"])

@@ -252,3 +252,16 @@ def test_entropy_is_reference_softmax_entropy():
     for c in _ext()["entropy"]:
         _, h = O.logsoftmax_row(np.asarray(c["row"], np.float64))
         assert abs(h - c["entropy"]) <= 1e-11 * max(1.0, abs(c["entropy"])), c["V"]
+
+
+def test_aggregation_and_dual_clip_identities_match_reference():
+    """seq-mean-token-mean and group-mean on equal-length unmasked batches, and
+    a never-binding dual-clip cap, reproduce the reference's token-mean loss."""
+    for c in _ext()["aggregation"]:
+        B, T = c["B"], c["T"]
+        lp = np.asarray(O.ref_logsoftmax_rows(np.asarray(c["row"]), [0], full=True)[1][0])[np.asarray(c["tokens"])]
+        for extra in (dict(loss_agg=1), dict(loss_agg=3, group_size=c["G"]), dict(dual_clip_c=1e9)):
+            oc = O.TrainConfig(**c["cfg"], **extra)
+            _, _, part = O.ppo_loss(oc, B, T, c["lengths"], None, lp, c["old"], c["ref"], c["adv"], np.zeros(B * T))
+            got = O.merge(part[None], oc)
+            assert abs(got["loss"] - c["ref_stats"]["loss"]) <= 1e-12 * max(1.0, abs(c["ref_stats"]["loss"])), extra
