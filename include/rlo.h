@@ -318,7 +318,10 @@ rlo_status rlo_batch_counts(rlo_handle* h, const rlo_train_config* cfg, const rl
 /* Actor backward epilogue (policy.cpp:375-379): for every row with
  * weight*dlogp != 0, grad[v] = weight*dlogp*(1[v == token] - exp(z_v - lse)),
  * recomputing the softmax from the row and its lse (never stored); all
- * other rows of `grad` are zeroed.  grad has grad_dtype (rlo_dtype) and
+ * other rows of `grad` are zeroed (with packed logits, rlo_logits.seq_start,
+ * gradient rows follow the same layout and only existing rows are written).
+ * The lse is fp32, so p carries its rounding (relative <= ulp(lse)/2: 4e-6 at
+ * |lse| < 64); the fused pass below has no such term.  grad has grad_dtype (rlo_dtype) and
  * grad_row_stride; lse / dlogp / weight are [B*T] (rlo_token_out.lse,
  * rlo_token_out.dlogp, rlo_loss_weights). */
 rlo_status rlo_logits_backward(rlo_handle* h, const rlo_batch* batch, const rlo_logits* logits, const float* lse,
@@ -333,8 +336,9 @@ rlo_status rlo_logits_backward(rlo_handle* h, const rlo_batch* batch, const rlo_
  * rows without loss participation get zeros.  weight [B*T] must be known
  * before the pass (rlo_batch_counts -> rlo_loss_weights).  HBM traffic per
  * participating row P*V*s + V*s_grad instead of (P+1)*V*s + V*s_grad.  Rows
- * that are not 16-byte aligned (or a vocabulary beyond 8 CTAs' shared memory)
- * take the two-pass form transparently. */
+ * that are not 16-byte aligned, or whose actor row needs more than 4 CTAs of
+ * 32 KB shared memory (e.g. the bf16 Qwen2.5 vocabulary, where the two-pass
+ * form is measured faster), take the two-pass form transparently. */
 rlo_status rlo_ppo_gradient_fused(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch,
                                   const rlo_logits* actor, const rlo_logits* old_logits, const rlo_logits* ref_logits,
                                   const float* old_logp, const float* ref_logp, const float* advantages,
@@ -356,7 +360,9 @@ rlo_status rlo_value_loss(rlo_handle* h, const rlo_batch* batch, const float* va
  * reference's keyed uniform u = keyed_double({seed, version, sample_key[i],
  * position[i]}) (rng.hpp:82-85), returning the token and its UNtempered
  * log-prob (policy.cpp:168), i.e. response_logprobs, so the PPO ratio needs
- * no separate old-policy logits pass.  fp64 internally, like the reference.
+ * no separate old-policy logits pass.  Tempered weights in fp64 like the
+ * reference (the token is the reference's unless u*total falls within fp64
+ * rounding of a CDF boundary); the untempered log-sum-exp in fp32.
  * sample_keys / positions [n_rows] device uint64; out_tokens int32 [n_rows];
  * out_logp float [n_rows].  ConfigError for temperature <= 0 (policy.cpp:146). */
 rlo_status rlo_decode_sample(rlo_handle* h, const rlo_logits* logits, int32_t n_rows, double temperature,
