@@ -335,10 +335,10 @@ rlo_status rlo_logits_backward(rlo_handle* h, const rlo_batch* batch, const rlo_
  * then writes grad[v] = weight*dlogp*(1[v == token] - softmax_v) from it;
  * rows without loss participation get zeros.  weight [B*T] must be known
  * before the pass (rlo_batch_counts -> rlo_loss_weights).  HBM traffic per
- * participating row P*V*s + V*s_grad instead of (P+1)*V*s + V*s_grad.  Rows
- * that are not 16-byte aligned, or whose actor row needs more than 4 CTAs of
- * 32 KB shared memory (e.g. the bf16 Qwen2.5 vocabulary, where the two-pass
- * form is measured faster), take the two-pass form transparently. */
+ * participating row P*V*s + V*s_grad instead of (P+1)*V*s + V*s_grad.  Runs
+ * for fp32 rows of <= 128 KB (4 CTAs of 32 KB shared memory); bf16 rows,
+ * larger rows and rows that are not 16-byte aligned take the two-pass form
+ * transparently (measured faster there). */
 rlo_status rlo_ppo_gradient_fused(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch* batch,
                                   const rlo_logits* actor, const rlo_logits* old_logits, const rlo_logits* ref_logits,
                                   const float* old_logp, const float* ref_logp, const float* advantages,

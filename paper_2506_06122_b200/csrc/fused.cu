@@ -399,10 +399,11 @@ cudaError_t launch_nt(const FusedArgs& f, int K, cudaStream_t s) {
 // rows not 16-byte aligned, or an actor row that needs more than
 // kMaxCluster CTAs of the slice budget.  Measured (profiles/r1_fused.txt):
 // fp32 V=32000 runs best as 4 CTAs x 32 KB slices (3 CTAs/SM) and beats the
-// two-pass form by 14%; the bf16 Qwen row (304 KB) needs 8 CTAs of 38 KB and
-// loses to the two-pass form (the per-row cluster barrier couples 8 SMs), so
-// it stays two-pass.  RLO_FUSED_SLICE_KB overrides the budget (and then allows
-// clusters up to 8) for experiments.
+// two-pass form by 12%.  bf16 rows lose to the two-pass form at every size
+// measured (V = 32000: 8.08 vs 7.59 ms; the Qwen row, 8 CTAs of 38 KB: 11.7 vs
+// 8.3 ms) — the bf16 pass is bound by SM power, not bytes — so bf16 stays
+// two-pass.  RLO_FUSED_SLICE_KB overrides the budget (and then allows any
+// dtype and clusters up to 8) for experiments.
 int fused_cluster_size(const VocabArgs& a, const void* grad, int32_t gdtype, int64_t gstride, int32_t* slice) {
   const int esz = a.dtype == RLO_DTYPE_BF16 ? 2 : 4, gsz = gdtype == RLO_DTYPE_BF16 ? 2 : 4;
   const int E = 16 / esz;
@@ -411,6 +412,7 @@ int fused_cluster_size(const VocabArgs& a, const void* grad, int32_t gdtype, int
   const int gal = E * gsz < 16 ? E * gsz : 16;  // widest gradient store
   if ((reinterpret_cast<uintptr_t>(grad) % gal) || ((gstride * gsz) % gal)) return 0;
   const int forced = vocab::env_int("RLO_FUSED_SLICE_KB", 0);
+  if (forced <= 0 && a.dtype == RLO_DTYPE_BF16) return 0;  // measured slower than two passes for bf16 (see above)
   const int64_t budget = (int64_t)(forced > 0 ? forced : 32) * 1024;
   const int kmax = forced > 0 ? 8 : 4;
   for (int K = 1; K <= kmax; K *= 2) {

@@ -18,6 +18,8 @@ import paper_2506_06122_b200 as rlo  # noqa: E402
 CASES = {
     "cfg2": dict(rows=131072, T=1024, V=32000, dt=torch.float32, gdt=torch.float32),
     "cfg3": dict(rows=32768, T=2048, V=152064, dt=torch.bfloat16, gdt=torch.bfloat16),
+    "bf16_32k": dict(rows=131072, T=1024, V=32000, dt=torch.bfloat16, gdt=torch.bfloat16),
+    "fp32_64k": dict(rows=65536, T=1024, V=65536, dt=torch.float32, gdt=torch.float32),
 }
 
 
