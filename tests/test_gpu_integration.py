@@ -27,3 +27,23 @@ def test_reference_workers_vs_b200_worker():
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.strip().endswith("OK (0 failures)")
+
+
+TRAINER = os.path.join(ROOT, "build", "trainer_step")
+
+
+def test_cpp_trainer_example_builds():
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "examples")], check=True)
+    assert os.path.exists(TRAINER)
+
+
+@pytest.mark.gpu
+def test_cpp_trainer_example_runs():
+    """A C++ trainer through include/rlo.hpp only: GRPO step over micro-batches,
+    the fused loss + dlogits pass (same loss), decode (examples/trainer_step.cpp)."""
+    if not os.path.exists(TRAINER):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "examples")], check=True)
+    r = subprocess.run([TRAINER], capture_output=True, text=True, timeout=300)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.strip().endswith("OK")
