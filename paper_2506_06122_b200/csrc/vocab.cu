@@ -42,7 +42,67 @@ constexpr int kWarps = kThreads / 32;
 #define RLO_ENT_GUARD_ALWAYS 0
 #endif
 
-template <typename ET, int NT, int U, bool PF, bool LOSS, bool ENT0, int MATH>
+// Lockstep streams (LS): the NT tensors of a row are streamed together, U
+// vectors of each per batch, and the old/ref states share the actor's running
+// max instead of taking their own chunk maxima (saves the per-chunk max and
+// rescale on NT-1 tensors — the bf16 pass is bound by SM power, so fewer
+// instructions per byte buy clock).  An old/ref element more than ~2^126 above
+// the actor's max would overflow its sum: such a thread's share (s non-finite
+// or 0) is redone with the tensor's own max.  Rows must all be 16-byte
+// aligned (else the sequential streams).
+template <typename ET, int NT, int U, int MATH>
+__device__ __forceinline__ void lockstep_accumulate(const ET* const (&rows)[NT], int V, Acc (&acc)[NT]) {
+  using VT = Vec<ET>;
+  using VV = typename VT::V;
+  constexpr int kStep = kThreads * U;
+  const int tid = threadIdx.x;
+  const int nvec = V / VT::kElems;
+  const int nfull = nvec / kStep * kStep;
+  auto step = [&](const VV (&v)[NT][U]) {
+    const float newmL = __fmul_rn(VT::template chunk_max<U>(v[0]), kL2E);
+    if (newmL > acc[0].mL) {  // rescale every state to the new shared max
+      const float d = acc[0].mL - newmL, sc = ex2(d);
+      acc[0].w = (acc[0].w + acc[0].s * d) * sc;
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        if (k) acc[k].s *= sc;
+        acc[k].mL = newmL;
+      }
+    }
+    VT::template accumulate<U, true, MATH | kMathNoMax>(v[0], acc[0]);
+#pragma unroll
+    for (int k = 1; k < NT; ++k) VT::template accumulate<U, false, MATH | kMathNoMax>(v[k], acc[k]);
+  };
+  for (int base = 0; base < nfull; base += kStep) {
+    VV v[NT][U];
+#pragma unroll
+    for (int k = 0; k < NT; ++k)
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[k][u] = ld_stream(reinterpret_cast<const VV*>(rows[k]) + base + u * kThreads + tid);
+    step(v);
+  }
+  if (nfull < nvec) {
+    VV v[NT][U];
+#pragma unroll
+    for (int k = 0; k < NT; ++k)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = nfull + u * kThreads + tid;
+        v[k][u] = idx < nvec ? ld_stream(reinterpret_cast<const VV*>(rows[k]) + idx) : VT::fill();
+      }
+    step(v);
+  }
+#pragma unroll
+  for (int k = 0; k < NT; ++k)
+    for (int i = nvec * VT::kElems + tid; i < V; i += kThreads) {
+      if (k == 0)
+        acc_scalar<ET, true>(rows[k] + i, acc[k]);
+      else
+        acc_scalar<ET, false>(rows[k] + i, acc[k]);
+    }
+}
+
+template <typename ET, int NT, int U, bool PF, bool LOSS, bool ENT0, int MATH, bool LS = false>
 __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel(const VocabArgs a) {
   __shared__ float red[2][kWarps][NT][3];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -58,6 +118,30 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
     float ztok[NT];
     if (tid == 0) gather_token<ET, NT>(a, row, tok, oov, ztok);
     Acc acc[NT];
+    if constexpr (LS && NT >= 2 && ENT0) {
+      const ET* rows[NT];
+      bool aligned = true;
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        rows[k] = reinterpret_cast<const ET*>(a.logits[k]) + logits_off(a, k, row);
+        aligned &= (reinterpret_cast<uintptr_t>(rows[k]) & 15u) == 0;
+        acc_init(acc[k]);
+      }
+      if (__all_sync(0xffffffffu, aligned)) {  // aligned is uniform per row anyway
+        lockstep_accumulate<ET, NT, U, MATH>(rows, a.V, acc);
+        if (!(isfinite(acc[0].s) && isfinite(acc[0].w))) {  // -inf logits in the actor share: guarded redo
+          acc_init(acc[0]);
+          stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rows[0], a.V, acc[0]);
+        }
+#pragma unroll
+        for (int k = 1; k < NT; ++k)
+          if (!(isfinite(acc[k].s) && acc[k].s > 0.f)) {  // above the shared max (or empty): own max
+            acc_init(acc[k]);
+            stream_accumulate<kThreads, ET, U, PF, false, MATH>(rows[k], a.V, acc[k]);
+          }
+        goto reduce;
+      }
+    }
 #pragma unroll
     for (int k = 0; k < NT; ++k) {
       acc_init(acc[k]);
@@ -77,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
       } else
         stream_accumulate<kThreads, ET, U, PF, false, MATH>(rp, a.V, acc[k]);
     }
+  reduce:
 #pragma unroll
     for (int k = 0; k < NT; ++k) {
       if (k == 0 && ENT0)
@@ -95,9 +180,9 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
   }
 }
 
-template <typename ET, int NT, bool LOSS, bool ENT0, int MATH, int U, bool PF>
+template <typename ET, int NT, bool LOSS, bool ENT0, int MATH, int U, bool PF, bool LS = false>
 cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
-  auto kern = vocab_ldg_kernel<ET, NT, U, PF, LOSS, ENT0, MATH>;
+  auto kern = vocab_ldg_kernel<ET, NT, U, PF, LOSS, ENT0, MATH, LS>;
   const int64_t nrows = (int64_t)a.B * a.T;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0);
@@ -134,6 +219,7 @@ cudaError_t launch_ldg_layout(const VocabArgs& a, int num_sms, cudaStream_t s) {
       case 1: return launch_ldg<ET, NT, LOSS, ENT0, MATH, 4, true>(a, num_sms, s);
       case 2: return launch_ldg<ET, NT, LOSS, ENT0, MATH, 8, false>(a, num_sms, s);
       case 3: return launch_ldg<ET, NT, LOSS, ENT0, MATH, 2, true>(a, num_sms, s);
+      case 4: return launch_ldg<ET, NT, LOSS, ENT0, MATH, 2, false, true>(a, num_sms, s);  // lockstep, U2 per tensor
       default: break;
     }
   }

@@ -102,6 +102,9 @@ __host__ __device__ constexpr int poly_deg_ent(int math) { return math == 4 ? 4 
 // Template MATH values may carry kMathGuard (the guarded entropy-row variant).
 constexpr int kMathMask = 0xff;
 constexpr int kMathGuard = 0x100;
+// kMathNoMax: the caller already rescaled the state to a shared running max
+// (lockstep streams of several tensors, vocab.cu); skip the per-chunk max.
+constexpr int kMathNoMax = 0x200;
 
 // GUARD (entropy row): clamp t so that -inf logits (masked vocabulary
 // entries) give e*t = 2^-126 * -126 (negligible) instead of 0 * -inf = NaN.
@@ -151,7 +154,7 @@ struct Vec<float> {
   __device__ static void accumulate(const V (&v)[U], Acc& a) {
     constexpr int MATH = MATHG & kMathMask;
     constexpr bool G = (MATHG & kMathGuard) != 0;
-    acc_rescale<ENT>(a, chunk_max<U>(v));
+    if (!(MATHG & kMathNoMax)) acc_rescale<ENT>(a, chunk_max<U>(v));
     if (MATH == 0) {
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, w0 = 0.f, w1 = 0.f, w2 = 0.f, w3 = 0.f;
 #pragma unroll
@@ -201,7 +204,7 @@ struct Vec<__nv_bfloat16> {
   __device__ static void accumulate(const V (&v)[U], Acc& a) {
     constexpr int MATH = MATHG & kMathMask;
     constexpr bool G = (MATHG & kMathGuard) != 0;
-    acc_rescale<ENT>(a, chunk_max<U>(v));
+    if (!(MATHG & kMathNoMax)) acc_rescale<ENT>(a, chunk_max<U>(v));
     if (MATH == 0) {
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, w0 = 0.f, w1 = 0.f, w2 = 0.f, w3 = 0.f;
 #pragma unroll

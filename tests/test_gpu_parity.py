@@ -255,6 +255,7 @@ def test_fused_loss_vs_oracle(env, dtype, agg, kl_est):
     ("tma", None, None), ("ldg", "0", None), ("tma", "0", None),                # fp32 mixes and producers
     ("ldg", "1", None), ("ldg", "2", None), ("ldg", "3", None), ("ldg", "4", None), ("ldg", "5", None),
     ("tma", "4", None), ("ldg", None, "1"), ("ldg", None, "2"), ("ldg", None, "3"),  # bf16 mixes / layouts
+    ("ldg", None, "4"), ("ldg", "4", "4"),                                         # bf16 lockstep streams
 ])
 def test_vocab_variants_vs_oracle(env, monkeypatch, impl, math, ldg):
     """Every selectable producer (LDG / TMA ring), instruction mix (RLO_VOCAB_MATH)
