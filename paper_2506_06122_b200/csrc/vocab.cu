@@ -180,6 +180,103 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
   }
 }
 
+// Epilogue-warp variant (RLO_VOCAB_EPI=1): 7 streaming warps + 1 epilogue
+// warp per 256-thread CTA.  The streaming warps hand each row's per-warp
+// partials to the epilogue warp through named barriers (RED: partials ready;
+// FREE: the double-buffered slot may be rewritten) and go straight on to the
+// next row; the epilogue warp gathers the token logits, combines, and runs the
+// fp64 loss epilogue.  In the default kernel the warp that runs row_finish
+// reaches the next row's __syncthreads late and the other warps wait for it
+// (ncu: ~11% of cfg2's warp samples at that barrier).
+constexpr int kEpiStreamWarps = 7;
+constexpr int kEpiStreamThreads = kEpiStreamWarps * 32;
+template <int ID>
+__device__ __forceinline__ void nb_arrive() { asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(kThreads) : "memory"); }
+template <int ID>
+__device__ __forceinline__ void nb_sync() { asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(kThreads) : "memory"); }
+
+template <typename ET, int NT, int U, bool LOSS, bool ENT0, int MATH>
+__global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_epi_kernel(const VocabArgs a) {
+  __shared__ float red[2][kEpiStreamWarps][NT][3];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool epi = warp == kEpiStreamWarps;
+  const int64_t nrows = (int64_t)a.B * a.T;
+  if (epi) {  // both slots start free
+    nb_arrive<1>();
+    nb_arrive<2>();
+  }
+  int buf = 0;
+  for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
+    if (!row_active<LOSS>(a, row, epi && lane == 0)) {  // uniform across the CTA
+      if (epi && lane == 0) write_inactive<LOSS>(a, row);
+      continue;
+    }
+    if (!epi) {
+      Acc acc[NT];
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        acc_init(acc[k]);
+        const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + logits_off(a, k, row);
+        if (k == 0 && ENT0) {
+          stream_accumulate<kEpiStreamThreads, ET, U, false, true, MATH>(rp, a.V, acc[k]);
+          if (!(isfinite(acc[k].s) && isfinite(acc[k].w))) {  // -inf logits: guarded redo of this share
+            acc_init(acc[k]);
+            stream_accumulate<kEpiStreamThreads, ET, U, false, true, MATH | kMathGuard>(rp, a.V, acc[k]);
+          }
+        } else {
+          stream_accumulate<kEpiStreamThreads, ET, U, false, false, MATH>(rp, a.V, acc[k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        if (k == 0 && ENT0)
+          acc_warp_reduce<true>(acc[k]);
+        else
+          acc_warp_reduce<false>(acc[k]);
+      }
+      if (buf) nb_sync<2>(); else nb_sync<1>();  // slot free (read by the epilogue two rows ago)
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < NT; ++k) {
+          red[buf][warp][k][0] = acc[k].mL;
+          red[buf][warp][k][1] = acc[k].s;
+          red[buf][warp][k][2] = acc[k].w;
+        }
+      }
+      if (buf) nb_arrive<4>(); else nb_arrive<3>();  // partials ready
+    } else {
+      int tok = 0;
+      bool oov = false;
+      float ztok[NT];
+      if (lane == 0) gather_token<ET, NT>(a, row, tok, oov, ztok);
+      if (buf) nb_sync<4>(); else nb_sync<3>();
+      Acc c[NT];
+      load_red<kEpiStreamWarps, NT>(red[buf], c, lane);
+      __syncwarp();
+      if (buf) nb_arrive<2>(); else nb_arrive<1>();  // slot read: free for row + 2
+      row_finish_acc<NT, LOSS, ENT0>(a, c, row, tok, oov, ztok, lane);
+    }
+    buf ^= 1;
+  }
+  if (!epi) {  // consume the epilogue warp's last two FREE arrivals (barrier phases stay balanced)
+    if (buf) nb_sync<2>(); else nb_sync<1>();
+    if (buf) nb_sync<1>(); else nb_sync<2>();
+  }
+}
+
+template <typename ET, int NT, bool LOSS, bool ENT0, int MATH, int U>
+cudaError_t launch_epi(const VocabArgs& a, int num_sms, cudaStream_t s) {
+  auto kern = vocab_epi_kernel<ET, NT, U, LOSS, ENT0, MATH>;
+  const int64_t nrows = (int64_t)a.B * a.T;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0);
+  int64_t grid = (int64_t)num_sms * (per_sm < 1 ? 1 : per_sm);
+  if (grid > nrows) grid = nrows;
+  kern<<<(int)grid, kThreads, 0, s>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
 template <typename ET, int NT, bool LOSS, bool ENT0, int MATH, int U, bool PF, bool LS = false>
 cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
   auto kern = vocab_ldg_kernel<ET, NT, U, PF, LOSS, ENT0, MATH, LS>;
@@ -230,6 +327,7 @@ template <typename ET, int NT, bool LOSS, bool ENT0, int MATH>
 cudaError_t launch_impl(const VocabArgs& a, int num_sms, cudaStream_t s) {
   if (use_tma((int)sizeof(ET)) && tma_eligible(a, (int)sizeof(ET)))
     return launch_tma<ET, NT, LOSS, ENT0, MATH>(a, num_sms, s);
+  if (env_int("RLO_VOCAB_EPI", 0)) return launch_epi<ET, NT, LOSS, ENT0, MATH, sizeof(ET) == 4 ? 8 : 4>(a, num_sms, s);
   return launch_ldg_layout<ET, NT, LOSS, ENT0, MATH>(a, num_sms, s);
 }
 

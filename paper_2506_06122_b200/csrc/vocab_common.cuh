@@ -471,26 +471,19 @@ __device__ __forceinline__ void gather_token(const VocabArgs& a, int64_t row, in
 }
 
 // Final cross-warp combine + outputs, executed by one full warp (all lanes):
-// red[w][k][0..2] holds warp w's (mL, s, w) for tensor k.
-template <int NT, int NWARPS, bool LOSS, bool ENT0>
-__device__ __forceinline__ void row_finish(const VocabArgs& a, const float (*red)[NT][3], int64_t row, int tok,
-                                           bool oov, const float (&ztok)[NT], int lane) {
+// lane w holds warp w's (mL, s, w) for each tensor in c[] (acc_init beyond the
+// warp count).
+template <int NT, bool LOSS, bool ENT0>
+__device__ __forceinline__ void row_finish_acc(const VocabArgs& a, Acc (&c)[NT], int64_t row, int tok, bool oov,
+                                               const float (&ztok)[NT], int lane) {
   double lse[NT], ent = 0.0;
 #pragma unroll
   for (int k = 0; k < NT; ++k) {
-    Acc c;
-    if (lane < NWARPS) {
-      c.mL = red[lane][k][0];
-      c.s = red[lane][k][1];
-      c.w = red[lane][k][2];
-    } else {
-      acc_init(c);
-    }
     if (k == 0 && ENT0)
-      acc_warp_reduce<true>(c);
+      acc_warp_reduce<true>(c[k]);
     else
-      acc_warp_reduce<false>(c);
-    const RowResult r = finish(c);
+      acc_warp_reduce<false>(c[k]);
+    const RowResult r = finish(c[k]);
     lse[k] = r.lse;
     if (k == 0) ent = r.entropy;
   }
@@ -507,6 +500,29 @@ __device__ __forceinline__ void row_finish(const VocabArgs& a, const float (*red
     return;
   }
   row_loss<NT>(a, row, lp, ent, lse[0], true);
+}
+
+// red[w][k][0..2] holds warp w's (mL, s, w) for tensor k.
+template <int NWARPS, int NT>
+__device__ __forceinline__ void load_red(const float (*red)[NT][3], Acc (&c)[NT], int lane) {
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    if (lane < NWARPS) {
+      c[k].mL = red[lane][k][0];
+      c[k].s = red[lane][k][1];
+      c[k].w = red[lane][k][2];
+    } else {
+      acc_init(c[k]);
+    }
+  }
+}
+
+template <int NT, int NWARPS, bool LOSS, bool ENT0>
+__device__ __forceinline__ void row_finish(const VocabArgs& a, const float (*red)[NT][3], int64_t row, int tok,
+                                           bool oov, const float (&ztok)[NT], int lane) {
+  Acc c[NT];
+  load_red<NWARPS, NT>(red, c, lane);
+  row_finish_acc<NT, LOSS, ENT0>(a, c, row, tok, oov, ztok, lane);
 }
 
 }  // namespace vocab

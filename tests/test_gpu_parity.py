@@ -256,12 +256,15 @@ def test_fused_loss_vs_oracle(env, dtype, agg, kl_est):
     ("ldg", "1", None), ("ldg", "2", None), ("ldg", "3", None), ("ldg", "4", None), ("ldg", "5", None),
     ("tma", "4", None), ("ldg", None, "1"), ("ldg", None, "2"), ("ldg", None, "3"),  # bf16 mixes / layouts
     ("ldg", None, "4"), ("ldg", "4", "4"),                                         # bf16 lockstep streams
+    ("epi", None, None), ("epi", "0", None),                                       # epilogue-warp kernel
 ])
 def test_vocab_variants_vs_oracle(env, monkeypatch, impl, math, ldg):
     """Every selectable producer (LDG / TMA ring), instruction mix (RLO_VOCAB_MATH)
     and LDG layout (RLO_VOCAB_LDG) against the oracle, both dtypes, with -inf
     entries in the actor rows (the guarded entropy redo)."""
-    monkeypatch.setenv("RLO_VOCAB_IMPL", impl)
+    monkeypatch.setenv("RLO_VOCAB_IMPL", "ldg" if impl == "epi" else impl)
+    if impl == "epi":
+        monkeypatch.setenv("RLO_VOCAB_EPI", "1")
     if math is not None:
         monkeypatch.setenv("RLO_VOCAB_MATH", math)
     if ldg is not None:
