@@ -3,15 +3,20 @@
 // sample.cpp:124-159; validation sample.cpp:85-102) parsed straight into the
 // padded host arrays the C ABI consumes.  Host-only C++: a small
 // recursive-descent JSON reader (objects, arrays, numbers, strings with
-// escapes, true/false/null) — numbers go through strtod, so values written by
-// the reference (round-trip precision) come back bit-exact.
+// escapes, true/false/null) — numbers go through std::from_chars (correctly
+// rounded), so values written by the reference (round-trip precision) come
+// back bit-exact; arrays of numbers are read straight into vectors.
+#include <algorithm>
+#include <charconv>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -25,7 +30,8 @@ struct JVal {
   bool b = false;
   double num = 0.0;
   std::string str;
-  std::vector<JVal> arr;
+  std::vector<JVal> arr;        // non-number elements of an array
+  std::vector<double> nums;     // number / bool elements of an array (no per-element JVal)
   std::vector<std::pair<std::string, JVal>> obj;
   const JVal* get(const char* key) const {
     for (const auto& kv : obj)
@@ -165,9 +171,19 @@ struct Parser {
         return true;
       }
       while (true) {
-        JVal child;
-        if (!value(child, depth + 1)) return false;
-        v.arr.push_back(std::move(child));
+        ws();
+        if (p < end && (*p == '-' || (*p >= '0' && *p <= '9'))) {  // fast path: numbers straight into nums
+          double x;
+          if (!number(x)) return false;
+          v.nums.push_back(x);
+        } else {
+          JVal child;
+          if (!value(child, depth + 1)) return false;
+          if (child.kind == JVal::Bool)
+            v.nums.push_back(child.b ? 1.0 : 0.0);
+          else
+            v.arr.push_back(std::move(child));
+        }
         ws();
         if (p < end && *p == ',') {
           ++p;
@@ -194,14 +210,18 @@ struct Parser {
       return lit("false");
     }
     if (c == 'n') return lit("null");
-    // number
-    std::string tok;
-    while (p < end && (std::strchr("+-0123456789.eE", *p) != nullptr)) tok += *p++;
-    if (tok.empty()) return fail("unexpected character");
-    char* e = nullptr;
     v.kind = JVal::Num;
-    v.num = std::strtod(tok.c_str(), &e);
-    if (!e || *e) return fail("bad number");
+    return number(v.num);
+  }
+  // A JSON number, correctly rounded (std::from_chars), so values written by
+  // the reference at round-trip precision come back bit-exact.
+  bool number(double& x) {
+    const char* q = p;
+    while (q < end && (std::strchr("+-0123456789.eE", *q) != nullptr)) ++q;
+    if (q == p) return fail("unexpected character");
+    const auto r = std::from_chars(p, q, x);
+    if (r.ec != std::errc() || r.ptr != q) return fail("bad number");
+    p = q;
     return true;
   }
 };
@@ -220,13 +240,11 @@ bool num_array(const JVal* v, std::vector<double>& out, std::string& err, const 
     err = std::string("'") + key + "' is not an array";
     return false;
   }
-  for (const auto& x : v->arr) {
-    if (x.kind != JVal::Num && x.kind != JVal::Bool) {
-      err = std::string("'") + key + "' holds a non-number";
-      return false;
-    }
-    out.push_back(x.kind == JVal::Bool ? (x.b ? 1.0 : 0.0) : x.num);
+  if (!v->arr.empty()) {  // any element that is neither a number nor a bool
+    err = std::string("'") + key + "' holds a non-number";
+    return false;
   }
+  out = v->nums;
   return true;
 }
 
@@ -244,6 +262,52 @@ T* alloc_fill(size_t n, T v) {
   T* p = static_cast<T*>(std::malloc(sizeof(T) * (n ? n : 1)));
   for (size_t i = 0; i < n; ++i) p[i] = v;
   return p;
+}
+
+// One JSONL line -> record (record_from_json, sample.cpp:124-140).  Returns
+// false with `err` set (the reference's message text) on a malformed line.
+bool parse_line(const char* p, const char* le, size_t line_no, Rec& r, std::string& err) {
+  Parser ps{p, le, {}};
+  JVal v;
+  if (!ps.value(v) || (ps.ws(), ps.p != le) || v.kind != JVal::Obj) {
+    err = "sample batch: malformed JSONL line " + std::to_string(line_no) + ": " +
+          (ps.err.empty() ? std::string("trailing characters or not an object") : ps.err);
+    return false;
+  }
+  if (const JVal* s = v.get("sample_id"); s && s->kind == JVal::Str) r.sample_id = s->str;
+  if (const JVal* s = v.get("group_id"); s && s->kind == JVal::Str) r.group_id = s->str;
+  std::string e;
+  if (!num_array(v.get("response_tokens"), r.response_tokens, e, "response_tokens") ||
+      !num_array(v.get("response_logprobs"), r.response_logprobs, e, "response_logprobs") ||
+      !num_array(v.get("ref_logprobs"), r.ref_logprobs, e, "ref_logprobs") ||
+      !num_array(v.get("rewards"), r.rewards, e, "rewards") ||
+      !num_array(v.get("advantages"), r.advantages, e, "advantages") ||
+      !num_array(v.get("action_mask"), r.action_mask, e, "action_mask")) {
+    err = "sample batch: line " + std::to_string(line_no) + ": " + e;
+    return false;
+  }
+  if (const JVal* s = v.get("scalar_reward"); s && s->kind == JVal::Num) {
+    r.has_scalar = true;
+    r.scalar = s->num;
+  }
+  return true;
+}
+
+// Worker threads for `n` independent items (RLO_JSONL_THREADS caps them; 1 =
+// serial).  Each worker takes a contiguous range, so per-item results keep
+// their order.
+template <class F>
+void parallel_ranges(size_t n, size_t min_per_thread, F&& f) {
+  size_t hw = std::max<unsigned>(1u, std::thread::hardware_concurrency());
+  if (const char* e = std::getenv("RLO_JSONL_THREADS"); e && *e) hw = std::max(1, std::atoi(e));
+  const size_t nt = std::max<size_t>(1, std::min(hw, n / std::max<size_t>(1, min_per_thread)));
+  if (nt <= 1) {
+    f(size_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (size_t k = 0; k < nt; ++k) th.emplace_back([&, k] { f(n * k / nt, n * (k + 1) / nt); });
+  for (auto& t : th) t.join();
 }
 
 }  // namespace
@@ -268,44 +332,44 @@ void rlo_host_batch_free(rlo_host_batch* b) {
 rlo_status rlo_batch_from_jsonl(const char* text, size_t len, rlo_host_batch** out) {
   if (!out) return set_last_error(RLO_ERR_INPUT, "batch_from_jsonl: null output");
   *out = nullptr;
-  std::vector<Rec> recs;
-  size_t line_no = 0;
+  // SampleBatch::from_jsonl: one record per non-empty line (sample.cpp:150-158).
+  // Lines are parsed in parallel; the first failing line (in line order) is
+  // reported, as the reference's sequential reader would.
+  std::vector<std::pair<const char*, const char*>> lines;
   const char* p = text;
   const char* end = text + (text ? len : 0);
-  while (p < end) {  // SampleBatch::from_jsonl: one record per non-empty line (sample.cpp:150-158)
+  while (p < end) {
     const char* nl = static_cast<const char*>(std::memchr(p, '\n', (size_t)(end - p)));
-    const char* le = nl ? nl : end;
-    ++line_no;
-    const char* q = p;
-    while (q < le && (*q == ' ' || *q == '\t' || *q == '\r')) ++q;
-    if (q < le) {
-      Parser ps{p, le, {}};
-      JVal v;
-      if (!ps.value(v) || (ps.ws(), ps.p != le) || v.kind != JVal::Obj) {
-        return set_last_error(RLO_ERR_INPUT, "sample batch: malformed JSONL line " + std::to_string(line_no) + ": " +
-                                                 (ps.err.empty() ? std::string("trailing characters or not an object")
-                                                                 : ps.err));
-      }
-      Rec r;
-      if (const JVal* s = v.get("sample_id"); s && s->kind == JVal::Str) r.sample_id = s->str;
-      if (const JVal* s = v.get("group_id"); s && s->kind == JVal::Str) r.group_id = s->str;
-      std::string err;
-      if (!num_array(v.get("response_tokens"), r.response_tokens, err, "response_tokens") ||
-          !num_array(v.get("response_logprobs"), r.response_logprobs, err, "response_logprobs") ||
-          !num_array(v.get("ref_logprobs"), r.ref_logprobs, err, "ref_logprobs") ||
-          !num_array(v.get("rewards"), r.rewards, err, "rewards") ||
-          !num_array(v.get("advantages"), r.advantages, err, "advantages") ||
-          !num_array(v.get("action_mask"), r.action_mask, err, "action_mask")) {
-        return set_last_error(RLO_ERR_INPUT, "sample batch: line " + std::to_string(line_no) + ": " + err);
-      }
-      if (const JVal* s = v.get("scalar_reward"); s && s->kind == JVal::Num) {
-        r.has_scalar = true;
-        r.scalar = s->num;
-      }
-      recs.push_back(std::move(r));
-    }
+    lines.emplace_back(p, nl ? nl : end);
     p = nl ? nl + 1 : end;
   }
+  std::vector<Rec> parsed(lines.size());
+  std::vector<char> present(lines.size(), 0);
+  std::vector<std::pair<size_t, std::string>> errors;  // (line index, message), first per worker
+  std::mutex mu;
+  parallel_ranges(lines.size(), 64, [&](size_t i0, size_t i1) {
+    for (size_t i = i0; i < i1; ++i) {
+      const char *q = lines[i].first, *le = lines[i].second;
+      while (q < le && (*q == ' ' || *q == '\t' || *q == '\r')) ++q;
+      if (q == le) continue;
+      std::string err;
+      if (!parse_line(lines[i].first, le, i + 1, parsed[i], err)) {
+        std::lock_guard<std::mutex> g(mu);
+        errors.emplace_back(i, std::move(err));
+        return;
+      }
+      present[i] = 1;
+    }
+  });
+  if (!errors.empty()) {
+    const auto first = std::min_element(errors.begin(), errors.end(),
+                                        [](const auto& a, const auto& b) { return a.first < b.first; });
+    return set_last_error(RLO_ERR_INPUT, first->second);
+  }
+  std::vector<Rec> recs;
+  recs.reserve(lines.size());
+  for (size_t i = 0; i < lines.size(); ++i)
+    if (present[i]) recs.push_back(std::move(parsed[i]));
   // SampleBatch::validate (sample.cpp:85-102), same messages
   std::set<std::string> ids;
   for (const auto& r : recs) {
@@ -354,26 +418,31 @@ rlo_status rlo_batch_from_jsonl(const char* text, size_t len, rlo_host_batch** o
   if (any_old) hb->response_logprobs = alloc_fill<float>(N, 0.f);
   if (any_ref) hb->ref_logprobs = alloc_fill<float>(N, 0.f);
   if (any_adv) hb->advantages = alloc_fill<float>(N, 0.f);
-  std::map<std::string, int32_t> groups;
+  std::map<std::string, int32_t> groups;  // group index in first-appearance order (sequential)
   for (int32_t b = 0; b < B; ++b) {
     const Rec& r = recs[static_cast<size_t>(b)];
-    const size_t n = r.response_tokens.size(), base = static_cast<size_t>(b) * T;
-    hb->lengths[b] = static_cast<int32_t>(n);
+    hb->lengths[b] = static_cast<int32_t>(r.response_tokens.size());
     hb->sample_keys[b] = fnv1a(r.sample_id);
-    auto g = groups.emplace(r.group_id, static_cast<int32_t>(groups.size()));
-    hb->group_index[b] = g.first->second;
-    for (size_t t = 0; t < n; ++t) {
-      hb->tokens[base + t] = static_cast<int32_t>(r.response_tokens[t]);
-      if (hb->mask) hb->mask[base + t] = r.action_mask.empty() ? 1 : (r.action_mask[t] != 0);
-      if (hb->response_logprobs && !r.response_logprobs.empty()) hb->response_logprobs[base + t] = (float)r.response_logprobs[t];
-      if (hb->ref_logprobs && !r.ref_logprobs.empty()) hb->ref_logprobs[base + t] = (float)r.ref_logprobs[t];
-      if (hb->advantages && !r.advantages.empty()) hb->advantages[base + t] = (float)r.advantages[t];
-      if (hb->rewards && !r.rewards.empty()) hb->rewards[base + t] = (float)r.rewards[t];
-    }
-    if (r.has_scalar && hb->scalar_rewards) hb->scalar_rewards[b] = (float)r.scalar;
-    if (hb->rewards && r.rewards.empty() && r.has_scalar && n > 0) hb->rewards[base + n - 1] = (float)r.scalar;
-    if (n > 0 && r.rewards.empty() && !r.has_scalar && hb->first_missing_reward < 0) hb->first_missing_reward = b;
+    hb->group_index[b] = groups.emplace(r.group_id, static_cast<int32_t>(groups.size())).first->second;
+    if (r.response_tokens.size() > 0 && r.rewards.empty() && !r.has_scalar && hb->first_missing_reward < 0)
+      hb->first_missing_reward = b;
   }
+  parallel_ranges(static_cast<size_t>(B), 16, [&](size_t b0, size_t b1) {  // the padded rows (independent)
+    for (size_t b = b0; b < b1; ++b) {
+      const Rec& r = recs[b];
+      const size_t n = r.response_tokens.size(), base = b * static_cast<size_t>(T);
+      for (size_t t = 0; t < n; ++t) {
+        hb->tokens[base + t] = static_cast<int32_t>(r.response_tokens[t]);
+        if (hb->mask) hb->mask[base + t] = r.action_mask.empty() ? 1 : (r.action_mask[t] != 0);
+        if (hb->response_logprobs && !r.response_logprobs.empty()) hb->response_logprobs[base + t] = (float)r.response_logprobs[t];
+        if (hb->ref_logprobs && !r.ref_logprobs.empty()) hb->ref_logprobs[base + t] = (float)r.ref_logprobs[t];
+        if (hb->advantages && !r.advantages.empty()) hb->advantages[base + t] = (float)r.advantages[t];
+        if (hb->rewards && !r.rewards.empty()) hb->rewards[base + t] = (float)r.rewards[t];
+      }
+      if (r.has_scalar && hb->scalar_rewards) hb->scalar_rewards[b] = (float)r.scalar;
+      if (hb->rewards && r.rewards.empty() && r.has_scalar && n > 0) hb->rewards[base + n - 1] = (float)r.scalar;
+    }
+  });
   *out = hb;
   return RLO_OK;
 }

@@ -70,40 +70,47 @@ def bench_value(obj):
                       "gbs": byts / ms / 1e6, "note": "includes the host sync of the stats"}), flush=True)
 
 
+def _big_jsonl(n, T, seed=5):
+    """A rollout batch the size the path consumes: n samples x T tokens with
+    old / ref log-probs (the reference's record keys, sample.cpp:124-140)."""
+    rng = np.random.default_rng(seed)
+    lines = []
+    for i in range(n):
+        toks = rng.integers(0, 152064, T)
+        lp = np.round(rng.uniform(-8, 0, T), 6)
+        ref = np.round(lp + rng.uniform(-0.1, 0.1, T), 6)
+        lines.append(json.dumps({"sample_id": f"s{i}", "group_id": f"g{i // 8}",
+                                 "response_tokens": toks.tolist(), "response_logprobs": lp.tolist(),
+                                 "ref_logprobs": ref.tolist(), "scalar_reward": float(rng.random() < 0.5)}))
+    return "\n".join(lines)
+
+
 def bench_jsonl():
     import oracle as O
-    n = 512
+    cases = []
     if O.ref_available():
-        text = O.ref_batch_jsonl(5, n)
-        src = "reference SampleBatch::to_jsonl"
-    else:
-        rng = np.random.default_rng(5)
-        lines = []
-        for i in range(n):
-            T = int(rng.integers(64, 512))
-            lines.append(json.dumps({"prompt_id": f"p{i // 8}", "sample_id": f"s{i}", "prompt": [1, 2, 3],
-                                     "response_tokens": rng.integers(0, 32000, T).tolist(),
-                                     "response_logprobs": rng.uniform(-5, 0, T).tolist(),
-                                     "scalar_reward": float(rng.random())}))
-        text = "\n".join(lines)
-        src = "synthetic"
-    mb = len(text.encode()) / 1e6
-    t0 = time.perf_counter()
-    k = 0
-    while time.perf_counter() - t0 < 2.0:
-        rlo.batch_from_jsonl(text)
-        k += 1
-    ours = (time.perf_counter() - t0) / k
-    out = {"row": "jsonl", "samples": n, "mb": mb, "source": src, "ms": ours * 1e3, "mb_per_s": mb / ours}
-    if O.ref_available():
-        t0 = time.perf_counter()
-        k = 0
-        while time.perf_counter() - t0 < 2.0:
-            O.ref_parse_validate_jsonl(text)
-            k += 1
-        ref = (time.perf_counter() - t0) / k
-        out.update(reference_ms=ref * 1e3, reference_mb_per_s=mb / ref, speedup=ref / ours)
-    print(json.dumps(out), flush=True)
+        cases.append(("reference SampleBatch::to_jsonl, 512 samples", O.ref_batch_jsonl(5, 512)))
+    cases.append(("synthetic 2048 samples x 1024 tokens", _big_jsonl(2048, 1024)))
+    for src, text in cases:
+        mb = len(text.encode()) / 1e6
+        data = text.encode()
+
+        def timeit(fn, budget=2.0):
+            t0, k = time.perf_counter(), 0
+            while k < 1 or time.perf_counter() - t0 < budget:
+                fn()
+                k += 1
+            return (time.perf_counter() - t0) / k
+        ours = timeit(lambda: rlo.batch_from_jsonl(data))
+        os.environ["RLO_JSONL_THREADS"] = "1"
+        serial = timeit(lambda: rlo.batch_from_jsonl(data))
+        del os.environ["RLO_JSONL_THREADS"]
+        out = {"row": "jsonl", "source": src, "mb": round(mb, 2), "ms": ours * 1e3, "mb_per_s": mb / ours,
+               "threads": os.cpu_count(), "serial_mb_per_s": mb / serial}
+        if O.ref_available():
+            ref = timeit(lambda: O.ref_parse_validate_jsonl(text))
+            out.update(reference_ms=ref * 1e3, reference_mb_per_s=mb / ref, speedup=ref / ours)
+        print(json.dumps(out), flush=True)
 
 
 def bench_broadcast():
