@@ -88,3 +88,23 @@ def test_bucket_plan_matches_reference():
     assert rlo.bucket_plan(1000, 256) == [256, 256, 256, 232]  # test_policy.cpp:499-500
     with pytest.raises(rlo.ConfigError):
         rlo.bucket_plan(10, 0)
+
+
+def test_jsonl_parallel_parse_reports_first_error_and_keeps_order(monkeypatch):
+    """Large batches are parsed on several threads: the records keep their line
+    order and the first malformed line (not the first one a thread meets) is
+    the one reported, as the reference's sequential reader would."""
+    lines = [json.dumps({"sample_id": f"s{i}", "group_id": f"g{i // 4}", "response_tokens": [i, i + 1, i + 2],
+                         "scalar_reward": float(i % 3)}) for i in range(2000)]
+    text = "\n".join(lines)
+    for threads in ("1", "8"):
+        monkeypatch.setenv("RLO_JSONL_THREADS", threads)
+        b = rlo.batch_from_jsonl(text)
+        assert b["B"] == 2000 and b["tokens"][1234].tolist() == [1234, 1235, 1236]
+        assert b["group_index"][1999] == 499 and b["scalar_rewards"][5] == 2.0
+    bad = list(lines)
+    bad[1700] = '{"sample_id": "x", "response_tokens": [1,]}'
+    bad[300] = '{"sample_id": "y", "response_tokens": [1, 2'
+    monkeypatch.setenv("RLO_JSONL_THREADS", "8")
+    with pytest.raises(rlo.InputError, match="malformed JSONL line 301:"):
+        rlo.batch_from_jsonl("\n".join(bad))
