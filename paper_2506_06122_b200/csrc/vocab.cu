@@ -291,8 +291,9 @@ cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
 }
 
 // Implementation / instruction-mix selection.  Defaults are the measured
-// best per dtype; RLO_VOCAB_IMPL=ldg|tma and
-// RLO_VOCAB_MATH=0..3 override them for experiments.
+// best per dtype (profiles/r1_vocab_sweep.txt); for
+// experiments RLO_VOCAB_IMPL=ldg|tma, RLO_VOCAB_MATH (fp32 0-1, bf16 1-6),
+// RLO_VOCAB_LDG (bf16 loss-pass layouts 1-4) and RLO_VOCAB_EPI=1 override them.
 int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return (e && *e) ? std::atoi(e) : dflt;
