@@ -129,3 +129,56 @@ def test_random_whole_path_vs_oracle(env, case):
         assert abs(getattr(st, k) - want[k]) <= 2e-5 * max(1.0, abs(want[k])), (case, k, getattr(st, k), want[k])
     for k in ("tokens", "seqs", "groups"):
         assert getattr(st, k) == want[k], (case, k)
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_random_update_pass_vs_oracle(env, case):
+    """Fused / two-pass actor update (whichever the entry picks) on random
+    shapes, padded or packed logits: gradient rows vs the oracle's
+    w*dlogp*(onehot - softmax), untouched padding."""
+    torch, rlo, obj = env
+    rng = np.random.default_rng(7000 + case)
+    B, T = int(rng.integers(1, 7)), int(rng.integers(1, 9))
+    V = int(rng.choice([8, 1000, 4096, 32000]))
+    dtype = torch.float32 if case % 3 else torch.bfloat16
+    P = int(rng.integers(1, 4))
+    packed = bool(case % 2)
+    lengths = rng.integers(0, T + 1, B).astype(np.int32)
+    lengths[0] = max(1, lengths[0])
+    mask = (rng.random((B, T)) < 0.85).astype(np.uint8)
+    tokens = rng.integers(0, V, (B, T)).astype(np.int32)
+    adv = rng.uniform(-1.5, 1.5, (B, T)).astype(np.float32)
+    gen = torch.Generator().manual_seed(case)
+    full = [(torch.randn(B * T, V, generator=gen) * 2).to(dtype)]
+    for _ in range(P - 1):
+        full.append((full[0].float() + torch.randn(B * T, V, generator=gen) * 0.1).to(dtype))
+    valid = np.concatenate([np.arange(b * T, b * T + lengths[b]) for b in range(B)])
+    start = np.concatenate([[0], np.cumsum(lengths)[:-1]]).astype(np.int64)
+    x = [(t[torch.from_numpy(valid)] if packed else t).contiguous().cuda() for t in full]
+    cfg = rlo.TrainConfig(loss_agg=int(rng.integers(0, 4)), group_size=1, kl_coef=0.01, kl_estimator="k3")
+    L, K, M, A = dev(torch, lengths), dev(torch, tokens), dev(torch, mask), dev(torch, adv)
+    cnt = obj.batch_counts(cfg, L, T, mask=M)
+    if cnt.tokens == 0:
+        return
+    w = obj.loss_weights(cfg, L, cnt, T, mask=M)
+    kw = dict(old_logits=x[1]) if P >= 2 else dict(old_logprobs=dev(torch, np.full((B, T), -6.0, np.float32)))
+    if P >= 3:
+        kw["ref_logits"] = x[2]
+    else:
+        kw["ref_logprobs"] = dev(torch, np.full((B, T), -6.0, np.float32))
+    nrows = len(valid) if packed else B * T
+    g = torch.full((nrows + 2, V), 777.0, device="cuda")
+    outs, _ = obj.ppo_gradient_fused(cfg, K, L, x[0], A, w, mask=M, grad=g[:nrows], outputs=("dlogp",),
+                                     seq_start=dev(torch, start) if packed else None, **kw)
+    obj.merge_gradients(cfg)
+    assert bool((g[nrows:] == 777.0).all())
+    G = g[:nrows].cpu().numpy()
+    rows = full[0].float().numpy().astype(np.float64)
+    dl, wv = outs["dlogp"].cpu().numpy().ravel(), w.cpu().numpy().ravel()
+    for j, r in enumerate(valid if packed else range(B * T)):
+        scale = float(np.float32(wv[r]) * np.float32(dl[r]))
+        if scale == 0.0:
+            assert not G[j].any()
+            continue
+        want = O.logits_backward_row(rows[r], int(tokens.ravel()[r]), scale)
+        assert np.abs(G[j] - want).max() <= 1e-5 * abs(scale) + 1e-12, (case, j)
