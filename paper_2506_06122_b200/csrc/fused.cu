@@ -157,19 +157,27 @@ template <int ID>
 __device__ __forceinline__ void bar_arrive_id() { asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(kFTotal) : "memory"); }
 template <int ID>
 __device__ __forceinline__ void bar_sync_id() { asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(kFTotal) : "memory"); }
-constexpr int kBarRed = 1, kBarBc = 3;
+// RED slot s uses barrier 1 + s, BC slot s uses 1 + NB + s (NB <= 3 slots)
 // immediate barrier ids (a register id makes ptxas reserve all 16)
 __device__ __forceinline__ void bar_arrive(int id) {
-  if (id == 1) bar_arrive_id<1>();
-  else if (id == 2) bar_arrive_id<2>();
-  else if (id == 3) bar_arrive_id<3>();
-  else bar_arrive_id<4>();
+  switch (id) {
+    case 1: bar_arrive_id<1>(); break;
+    case 2: bar_arrive_id<2>(); break;
+    case 3: bar_arrive_id<3>(); break;
+    case 4: bar_arrive_id<4>(); break;
+    case 5: bar_arrive_id<5>(); break;
+    default: bar_arrive_id<6>(); break;
+  }
 }
 __device__ __forceinline__ void bar_sync(int id) {
-  if (id == 1) bar_sync_id<1>();
-  else if (id == 2) bar_sync_id<2>();
-  else if (id == 3) bar_sync_id<3>();
-  else bar_sync_id<4>();
+  switch (id) {
+    case 1: bar_sync_id<1>(); break;
+    case 2: bar_sync_id<2>(); break;
+    case 3: bar_sync_id<3>(); break;
+    case 4: bar_sync_id<4>(); break;
+    case 5: bar_sync_id<5>(); break;
+    default: bar_sync_id<6>(); break;
+  }
 }
 
 // Warp-specialised and software-pipelined over the cluster's rows.
@@ -189,13 +197,14 @@ __device__ __forceinline__ void bar_sync(int id) {
 // iteration i+2 only after every peer's epilogue warp has arrived for phase
 // i+1, i.e. after it read phase i's slots.  Only the epilogue warp writes
 // part, so only it arrives with release semantics.
-template <typename ET, typename GT, int NT, int U, int MATH>
+template <typename ET, typename GT, int NT, int U, int MATH, int NB>
 __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
+  constexpr int kRed = 1, kBc = 1 + NB;
   using VV = typename Vec<ET>::V;
   extern __shared__ __align__(16) unsigned char smraw[];
-  __shared__ float part[2][NT][3];  // this CTA's partial state per tensor, read by the cluster over DSMEM
-  __shared__ float red[2][kFW][NT][3];
-  __shared__ float bc[2][4];  // per row: mL, -scale/s, scale, token offset in this slice
+  __shared__ float part[NB][NT][3];  // this CTA's partial state per tensor, read by the cluster over DSMEM
+  __shared__ float red[NB][kFW][NT][3];
+  __shared__ float bc[NB][4];  // per row: mL, -scale/s, scale, token offset in this slice
   cg::cluster_group cl = cg::this_cluster();
   const int K = (int)cl.num_blocks(), r = (int)cl.block_rank();
   const VocabArgs& a = f.v;
@@ -205,8 +214,8 @@ __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
   const int64_t ncl = gridDim.x / K;
   const int c0 = r * f.slice;
   const int n = max(0, min(a.V - c0, f.slice));
-  VV* const smb0 = reinterpret_cast<VV*>(smraw);
-  VV* const smb1 = smb0 + f.slice / Vec<ET>::kElems;
+  VV* const smb = reinterpret_cast<VV*>(smraw);  // NB actor slices
+  const int slice_vecs = f.slice / Vec<ET>::kElems;
   // Next loss-participating row of this cluster at or after `row` (the same
   // for every CTA of the cluster); rows passed over get their zero gradient
   // slice (streaming warps) and inactive outputs here.
@@ -222,14 +231,17 @@ __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
   };
   auto backward = [&](int64_t row, int b) {
     const float* q = bc[b];
-    slice_grad<ET, GT>(reinterpret_cast<const ET*>(a.logits[0]) + logits_off(a, 0, row) + c0, n, b ? smb1 : smb0,
-                       grad_row(row), q[0], q[1], __float_as_int(q[3]), q[2]);
+    slice_grad<ET, GT>(reinterpret_cast<const ET*>(a.logits[0]) + logits_off(a, 0, row) + c0, n,
+                       smb + b * slice_vecs, grad_row(row), q[0], q[1], __float_as_int(q[3]), q[2]);
   };
+  int64_t pend[NB];  // row streamed into slot s, awaiting its gradient (-1: none)
+#pragma unroll
+  for (int s = 0; s < NB; ++s) pend[s] = -1;
   int64_t prev = -1;
   int b = 0;
-  for (int64_t row = next_active(blockIdx.x / K); row < nrows; row = next_active(row + ncl), b ^= 1) {
+  for (int64_t row = next_active(blockIdx.x / K); row < nrows; row = next_active(row + ncl), b = (b + 1) % NB) {
     if (!epi) {
-      VV* sm = b ? smb1 : smb0;
+      VV* sm = smb + b * slice_vecs;
       const ET* rp0 = reinterpret_cast<const ET*>(a.logits[0]) + logits_off(a, 0, row) + c0;
       Acc acc[NT];
 #pragma unroll
@@ -258,19 +270,22 @@ __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
           red[b][warp][k][2] = acc[k].w;
         }
       }
-      bar_arrive(kBarRed + b);
+      bar_arrive(kRed + b);
       if (prev >= 0) cluster_wait();  // phase of row prev (one phase of slack)
       cluster_arrive_relaxed();        // phase of row `row`
-      if (prev >= 0) {
-        bar_sync(kBarBc + (b ^ 1));  // row prev's epilogue
-        backward(prev, b ^ 1);
+      const int sb = (b + 1) % NB;     // oldest pending slot: the row of NB-1 iterations ago
+      if (pend[sb] >= 0) {
+        bar_sync(kBc + sb);  // that row's epilogue
+        backward(pend[sb], sb);
+        pend[sb] = -1;
       }
+      pend[b] = row;
     } else {
       int tok = 0;
       bool oov = false;
       float ztok[NT];
       if (lane == 0) gather_token<ET, NT>(a, row, tok, oov, ztok);
-      bar_sync(kBarRed + b);
+      bar_sync(kRed + b);
 #pragma unroll
       for (int k = 0; k < NT; ++k) {
         Acc c;
@@ -332,14 +347,20 @@ __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
         bc[b][3] = __int_as_float(tok - c0);
       }
       __syncwarp();
-      bar_arrive(kBarBc + b);
+      bar_arrive(kBc + b);
     }
     prev = row;
   }
   if (!epi && prev >= 0) {
     cluster_wait();  // the last phase
-    bar_sync(kBarBc + (b ^ 1));
-    backward(prev, b ^ 1);
+#pragma unroll
+    for (int j = 1; j <= NB; ++j) {  // the remaining rows, oldest first
+      const int sb = (b + j) % NB;
+      if (pend[sb] >= 0) {
+        bar_sync(kBc + sb);
+        backward(pend[sb], sb);
+      }
+    }
   }
   cl.sync();  // DSMEM lifetime: no CTA exits while a peer may still read its slots
 }
@@ -349,12 +370,12 @@ int env_int(const char* name, int dflt) {
   return (e && *e) ? std::atoi(e) : dflt;
 }
 
-template <typename ET, typename GT, int NT>
+template <typename ET, typename GT, int NT, int NB>
 cudaError_t launch_t(const FusedArgs& f, int K, cudaStream_t s) {
   constexpr int U = sizeof(ET) == 4 ? 8 : 4;
   constexpr int MATH = sizeof(ET) == 4 ? 1 : 6;  // the vocab pass's measured defaults
-  auto kern = fused_kernel<ET, GT, NT, U, MATH>;
-  const size_t smem = (size_t)f.slice * sizeof(ET) * 2;  // double-buffered actor slice
+  auto kern = fused_kernel<ET, GT, NT, U, MATH, NB>;
+  const size_t smem = (size_t)f.slice * sizeof(ET) * NB;  // NB actor slices in flight
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchAttribute attr[1];
@@ -383,13 +404,21 @@ cudaError_t launch_t(const FusedArgs& f, int K, cudaStream_t s) {
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+template <typename ET, typename GT, int NB>
+cudaError_t launch_nb(const FusedArgs& f, int K, cudaStream_t s) {
+  switch (f.v.ntens) {
+    case 1: return launch_t<ET, GT, 1, NB>(f, K, s);
+    case 2: return launch_t<ET, GT, 2, NB>(f, K, s);
+    default: return launch_t<ET, GT, 3, NB>(f, K, s);
+  }
+}
+
+// RLO_FUSED_NB=3: the gradient of a row is written two rows later (three
+// actor slices in flight), giving the epilogue and the cluster another row of
+// slack at the cost of shared memory (A/B knob, profiles/r1_fused.txt).
 template <typename ET, typename GT>
 cudaError_t launch_nt(const FusedArgs& f, int K, cudaStream_t s) {
-  switch (f.v.ntens) {
-    case 1: return launch_t<ET, GT, 1>(f, K, s);
-    case 2: return launch_t<ET, GT, 2>(f, K, s);
-    default: return launch_t<ET, GT, 3>(f, K, s);
-  }
+  return env_int("RLO_FUSED_NB", 2) == 3 ? launch_nb<ET, GT, 3>(f, K, s) : launch_nb<ET, GT, 2>(f, K, s);
 }
 
 }  // namespace
