@@ -193,3 +193,10 @@ def test_fused_errors(env):
         obj.sync()
     with pytest.raises((rlo.TrainingError, rlo.InputError)):
         obj.merge_gradients(cfg)  # the OOV row's NaN log-prob makes the loss non-finite
+
+
+def test_fused_three_slices_in_flight(env, monkeypatch):
+    """RLO_FUSED_NB=3 (gradient written two rows late) gives the same results."""
+    monkeypatch.setenv("RLO_FUSED_NB", "3")
+    test_fused_matches_two_pass_and_oracle(env, "f32", "f32", 32000, 3, 1)
+    test_fused_matches_two_pass_and_oracle(env, "f32", "bf16", 4099, 1, 3)
