@@ -65,7 +65,7 @@ __device__ __forceinline__ void lockstep_accumulate(const ET* const (&rows)[NT],
       acc[0].w = (acc[0].w + acc[0].s * d) * sc;
 #pragma unroll
       for (int k = 0; k < NT; ++k) {
-        if (k) acc[k].s *= sc;
+        acc[k].s *= sc;
         acc[k].mL = newmL;
       }
     }

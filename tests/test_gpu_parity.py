@@ -276,7 +276,7 @@ def test_vocab_variants_vs_oracle(env, monkeypatch, impl, math, ldg):
             continue
         torch, rlo, obj = env
         rng = np.random.default_rng(77)
-        B, T, V = 6, 9, 4096
+        B, T, V = 6, 9, 4096 if dtype == O.F32 else 16384  # several load batches per row on every path
         lengths, tokens, mask, adv, rows = _random_case(rng, B, T, V, dtype)
         ninf, half = (-np.inf, 0.5) if dtype == O.F32 else (0xFF80, 0x3F00)  # bf16 bit patterns
         rows[0][3, ::7] = ninf
