@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kThreadsTma, 1) vocab_tma_kernel(const VocabAr
 #pragma unroll 1
         for (int k = 0; k < NT; ++k) {
           const char* src =
-              reinterpret_cast<const char*>(a.logits[k]) + row * a.stride[k] * (int64_t)sizeof(ET);
+              reinterpret_cast<const char*>(a.logits[k]) + logits_off(a, k, row) * (int64_t)sizeof(ET);
           for (int c = 0; c < nchunks; ++c) {
             const int64_t rem = rowbytes - (int64_t)c * kChunk;
             const uint32_t bytes = (uint32_t)(rem < kChunk ? rem : kChunk);
@@ -197,7 +197,6 @@ bool tma_eligible(const VocabArgs& a, int esz) {
   for (int k = 0; k < a.ntens; ++k) {
     if ((reinterpret_cast<uintptr_t>(a.logits[k]) & 15u) != 0) return false;
     if ((a.stride[k] * esz) % 16 != 0) return false;
-    if (a.seq_start[k]) return false;  // packed logits: the LDG kernel
   }
   return true;
 }
