@@ -57,6 +57,8 @@ def _kw(torch, P, x, old, ref):
 @pytest.mark.parametrize("dt,gdt,V,P", [
     ("f32", "f32", 32000, 3),   # cfg 1-2 vocabulary: 2-CTA cluster
     ("f32", "f32", 4099, 1),    # odd V: the last slice's scalar tail
+    ("f32", "f32", 10000, 2),   # 2-CTA cluster
+    ("f32", "bf16", 20008, 3),  # 4-CTA cluster, uneven last slice
     ("f32", "bf16", 5000, 2),
     ("bf16", "bf16", 152064, 3),  # Qwen2.5 vocabulary: 4-CTA cluster
     ("bf16", "f32", 2051, 1),
