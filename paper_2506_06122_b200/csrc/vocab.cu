@@ -264,6 +264,104 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_epi_kernel
   }
 }
 
+// Barrier-free variant (RLO_VOCAB_LF=1): the per-warp partials of a row go
+// to one of kLfSlots shared-memory slots, each warp announces itself with an
+// atomicAdd on the slot's arrival counter, and the LAST warp to arrive
+// combines the row and runs the fp64 epilogue — nobody waits for it, and no
+// warp waits at a per-row __syncthreads for the one that finished the
+// previous row.  A slot is reused kLfSlots rows later; a writer spins (shared
+// memory, same CTA) until the slot's previous finisher has read it, which it
+// almost never has to.
+constexpr int kLfSlots = 4;
+
+template <typename ET, int NT, int U, bool LOSS, bool ENT0, int MATH>
+__global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_lf_kernel(const VocabArgs a) {
+  __shared__ float red[kLfSlots][kWarps][NT][3];
+  __shared__ int arrivals[kLfSlots];
+  __shared__ int done[kLfSlots];  // completed uses of the slot (rows finished from it)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t nrows = (int64_t)a.B * a.T;
+  if (tid < kLfSlots) {
+    arrivals[tid] = 0;
+    done[tid] = 0;
+  }
+  __syncthreads();
+  int j = 0;  // this CTA's active-row counter
+  for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
+    if (!row_active<LOSS>(a, row, tid == 0)) {  // uniform across the CTA
+      if (tid == 0) write_inactive<LOSS>(a, row);
+      continue;
+    }
+    Acc acc[NT];
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      acc_init(acc[k]);
+      const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + logits_off(a, k, row);
+      if (k == 0 && ENT0) {
+        stream_accumulate<kThreads, ET, U, false, true, MATH>(rp, a.V, acc[k]);
+        if (!(isfinite(acc[k].s) && isfinite(acc[k].w))) {  // -inf logits: guarded redo of this share
+          acc_init(acc[k]);
+          stream_accumulate<kThreads, ET, U, false, true, MATH | kMathGuard>(rp, a.V, acc[k]);
+        }
+      } else {
+        stream_accumulate<kThreads, ET, U, false, false, MATH>(rp, a.V, acc[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      if (k == 0 && ENT0)
+        acc_warp_reduce<true>(acc[k]);
+      else
+        acc_warp_reduce<false>(acc[k]);
+    }
+    const int slot = j % kLfSlots, use = j / kLfSlots;
+    int last = 0;
+    if (lane == 0) {
+      while (*reinterpret_cast<volatile int*>(&done[slot]) < use) {
+      }  // the slot's previous row has been read by its finisher
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        red[slot][warp][k][0] = acc[k].mL;
+        red[slot][warp][k][1] = acc[k].s;
+        red[slot][warp][k][2] = acc[k].w;
+      }
+      __threadfence_block();  // release the partials
+      last = atomicAdd(&arrivals[slot], 1) == kWarps - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {  // the final arrival finishes the row
+      __threadfence_block();  // acquire the other warps' partials
+      int tok = 0;
+      bool oov = false;
+      float ztok[NT];
+      if (lane == 0) gather_token<ET, NT>(a, row, tok, oov, ztok);
+      Acc c[NT];
+      load_red<kWarps, NT>(red[slot], c, lane);
+      __syncwarp();
+      if (lane == 0) {
+        arrivals[slot] = 0;
+        __threadfence_block();
+        atomicAdd(&done[slot], 1);  // slot free for row j + kLfSlots
+      }
+      row_finish_acc<NT, LOSS, ENT0>(a, c, row, tok, oov, ztok, lane);
+    }
+    ++j;
+  }
+}
+
+template <typename ET, int NT, bool LOSS, bool ENT0, int MATH, int U>
+cudaError_t launch_lf(const VocabArgs& a, int num_sms, cudaStream_t s) {
+  auto kern = vocab_lf_kernel<ET, NT, U, LOSS, ENT0, MATH>;
+  const int64_t nrows = (int64_t)a.B * a.T;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0);
+  int64_t grid = (int64_t)num_sms * (per_sm < 1 ? 1 : per_sm);
+  if (grid > nrows) grid = nrows;
+  kern<<<(int)grid, kThreads, 0, s>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
 template <typename ET, int NT, bool LOSS, bool ENT0, int MATH, int U>
 cudaError_t launch_epi(const VocabArgs& a, int num_sms, cudaStream_t s) {
   auto kern = vocab_epi_kernel<ET, NT, U, LOSS, ENT0, MATH>;
@@ -329,6 +427,7 @@ cudaError_t launch_impl(const VocabArgs& a, int num_sms, cudaStream_t s) {
   if (use_tma((int)sizeof(ET)) && tma_eligible(a, (int)sizeof(ET)))
     return launch_tma<ET, NT, LOSS, ENT0, MATH>(a, num_sms, s);
   if (env_int("RLO_VOCAB_EPI", 0)) return launch_epi<ET, NT, LOSS, ENT0, MATH, sizeof(ET) == 4 ? 8 : 4>(a, num_sms, s);
+  if (env_int("RLO_VOCAB_LF", 0)) return launch_lf<ET, NT, LOSS, ENT0, MATH, sizeof(ET) == 4 ? 8 : 4>(a, num_sms, s);
   return launch_ldg_layout<ET, NT, LOSS, ENT0, MATH>(a, num_sms, s);
 }
 
