@@ -39,7 +39,7 @@ extern "C" {
 #pragma GCC visibility push(default) /* the library is built -fvisibility=hidden; export exactly this header */
 #endif
 
-#define RLO_ABI_VERSION 2
+#define RLO_ABI_VERSION 3
 
 /* Status codes — reference exception taxonomy (include/rollmini/errors.hpp). */
 typedef enum rlo_status {
@@ -152,6 +152,21 @@ typedef struct rlo_stats {
   uint64_t groups;           /* groups with >= 1 participating token */
 } rlo_stats;
 
+/* Result of rlo_merge_gradients_async, written by the device (no host
+ * synchronisation, so a whole step can be captured in a CUDA graph).
+ * status: 0 ok, else the rlo_status merge_gradients would have returned
+ * (with the reason in `reason`: 1 no loss-participating tokens, 2 non-finite
+ * gradient, 3 non-finite loss, 4 a device-side input error — `dev_error` /
+ * `dev_error_value` as reported by the kernels).  rlo_step_result_check()
+ * turns a host copy into the same status and message. */
+typedef struct rlo_step_result {
+  rlo_stats stats;
+  int32_t status;
+  int32_t reason;
+  int32_t dev_error;
+  int32_t dev_error_value;
+} rlo_step_result;
+
 /* Per-rank partial sums: the scalar part of GradAccum (policy.hpp:121-128),
  * extended.  Merged in rank order exactly like merge_gradients
  * (policy.cpp:428-436).  Layout of v[] (all fp64; counts are exact integers): */
@@ -260,6 +275,19 @@ rlo_status rlo_ppo_gradient(rlo_handle* h, const rlo_train_config* cfg, const rl
  * accumulator.  out_partials (this rank's, optional) may be NULL. */
 rlo_status rlo_merge_gradients(rlo_handle* h, const rlo_train_config* cfg, rlo_stats* out,
                                rlo_partials* out_partials, void* stream);
+
+/* merge_gradients without host synchronisation: the accumulated sequences
+ * are reduced, all-gathered over the communicator (NCCL on `stream`) and
+ * merged in rank order on the device into `out` (device or host-mapped
+ * memory).  Every launch is capturable: warm the handle up with one eager
+ * step of the same shapes, then capture compute_advantages -> ppo_gradient ->
+ * merge_gradients_async in a CUDA graph and replay it (launch-bound small
+ * batches).  Errors are reported in out->status, not returned. */
+rlo_status rlo_merge_gradients_async(rlo_handle* h, const rlo_train_config* cfg, rlo_step_result* out, void* stream);
+
+/* Status (and rlo_last_error message) of a host copy of an rlo_step_result:
+ * exactly what the synchronous rlo_merge_gradients would have returned. */
+rlo_status rlo_step_result_check(const rlo_step_result* host_result);
 
 /* The rank-local GradAccum scalars of everything accumulated since the last
  * merge (what ppo_gradient returns per rank, policy.hpp:141): fixed-order

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # RLO_LIB overrides the in-tree library (A/B builds of the same sources in kernel experiments).
 LIB_PATH = os.environ.get("RLO_LIB") or os.path.join(HERE, "lib", "librlo.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "rlo.h")
-ABI_VERSION = 2  # include/rlo.h RLO_ABI_VERSION: the struct layouts below
+ABI_VERSION = 3  # include/rlo.h RLO_ABI_VERSION: the struct layouts below
 
 RLO_OK, RLO_ERR_INPUT, RLO_ERR_CONFIG, RLO_ERR_TRAINING, RLO_ERR_CUDA, RLO_ERR_NCCL, RLO_ERR_DISPATCH = range(7)
 DTYPE_F32, DTYPE_BF16 = 0, 1
@@ -55,6 +55,11 @@ class rlo_stats(C.Structure):
         ("mean_kl", C.c_double), ("tokens", C.c_uint64), ("mean_entropy", C.c_double),
         ("dual_clip_fraction", C.c_double), ("seqs", C.c_uint64), ("groups", C.c_uint64),
     ]
+
+
+class rlo_step_result(C.Structure):
+    _fields_ = [("stats", rlo_stats), ("status", C.c_int32), ("reason", C.c_int32), ("dev_error", C.c_int32),
+                ("dev_error_value", C.c_int32)]
 
 
 class rlo_value_stats(C.Structure):
@@ -118,6 +123,8 @@ def lib() -> C.CDLL:
                               P(rlo_logits), vp, vp, vp, P(rlo_token_out), vp], C.c_int),
         "rlo_merge_gradients": ([vp, P(rlo_train_config), P(rlo_stats), P(rlo_partials), vp], C.c_int),
         "rlo_rank_partials": ([vp, P(rlo_train_config), P(rlo_partials), vp], C.c_int),
+        "rlo_merge_gradients_async": ([vp, P(rlo_train_config), vp, vp], C.c_int),
+        "rlo_step_result_check": ([P(rlo_step_result)], C.c_int),
         "rlo_objective_step": ([vp, P(rlo_train_config), P(rlo_batch), vp, vp, vp, P(rlo_logits), P(rlo_logits),
                                 P(rlo_logits), vp, vp, vp, P(rlo_token_out), P(rlo_stats), vp], C.c_int),
         "rlo_objective_step_host": ([vp, P(rlo_train_config), i32, i32, vp, vp, vp, vp, vp, vp, P(rlo_logits),

@@ -263,33 +263,17 @@ rlo_status rlo_shard_plan(int32_t B, int32_t G, int32_t world, int32_t rank, int
 rlo_status rlo_merge_partials(const rlo_partials* parts, int32_t nranks, const rlo_train_config* cfg, rlo_stats* out) {
   // merge_gradients, policy.cpp:421-450: rank-ordered sums, then normalisation.
   if (nranks <= 0 || !parts) return fail(RLO_ERR_TRAINING, "merge_gradients: no gradient parts");
-  double s[RLO_NPARTIAL] = {0};
-  for (int32_t r = 0; r < nranks; ++r)
-    for (int k = 0; k < RLO_NPARTIAL; ++k) s[k] += parts[r].v[k];
-  if (s[RLO_P_TOKENS] == 0.0)
-    return fail(RLO_ERR_TRAINING, "merge_gradients: batch contains no loss-participating tokens");
-  if (s[RLO_P_NONFINITE_GRAD] > 0.0) return fail(RLO_ERR_TRAINING, "training step aborted: non-finite gradient");
-  const double inv = 1.0 / s[RLO_P_TOKENS];
+  std::vector<double> flat(static_cast<size_t>(nranks) * RLO_NPARTIAL);
+  for (int32_t r = 0; r < nranks; ++r) std::memcpy(&flat[static_cast<size_t>(r) * RLO_NPARTIAL], parts[r].v,
+                                                   sizeof(double) * RLO_NPARTIAL);
   rlo_stats st;
   std::memset(&st, 0, sizeof(st));
-  const int agg = cfg ? cfg->loss_agg : RLO_AGG_TOKEN_MEAN;
-  if (agg == RLO_AGG_SEQ_MEAN_TOKEN_MEAN)
-    st.loss = s[RLO_P_SEQ_MEAN_SUM] * (1.0 / s[RLO_P_SEQS]);
-  else if (agg == RLO_AGG_SEQ_MEAN_TOKEN_SUM)
-    st.loss = s[RLO_P_LOSS_SUM] * (1.0 / s[RLO_P_SEQS]);
-  else if (agg == RLO_AGG_GROUP_MEAN)
-    st.loss = s[RLO_P_GROUP_MEAN_SUM] * (1.0 / s[RLO_P_GROUPS]);
-  else
-    st.loss = s[RLO_P_LOSS_SUM] * inv;
-  st.mean_ratio = s[RLO_P_RATIO_SUM] * inv;
-  st.clip_fraction = s[RLO_P_CLIPPED] * inv;
-  st.mean_kl = s[RLO_P_KL_SUM] * inv;
-  st.tokens = static_cast<uint64_t>(s[RLO_P_TOKENS]);
-  st.mean_entropy = s[RLO_P_ENTROPY_SUM] * inv;
-  st.dual_clip_fraction = s[RLO_P_DUAL_CLIPPED] * inv;
-  st.seqs = static_cast<uint64_t>(s[RLO_P_SEQS]);
-  st.groups = static_cast<uint64_t>(s[RLO_P_GROUPS]);
-  if (!std::isfinite(st.loss)) return fail(RLO_ERR_TRAINING, "training step aborted: non-finite loss");
+  switch (merge_stats(flat.data(), nranks, cfg ? cfg->loss_agg : RLO_AGG_TOKEN_MEAN, &st)) {
+    case 1: return fail(RLO_ERR_TRAINING, "merge_gradients: batch contains no loss-participating tokens");
+    case 2: return fail(RLO_ERR_TRAINING, "training step aborted: non-finite gradient");
+    case 3: return fail(RLO_ERR_TRAINING, "training step aborted: non-finite loss");
+    default: break;
+  }
   if (out) *out = st;
   return RLO_OK;
 }
@@ -417,10 +401,7 @@ rlo_status check_logits(const rlo_logits* l, const char* op, const char* which) 
   return RLO_OK;
 }
 
-rlo_status collect_device_error(rlo_handle* h, cudaStream_t s) {
-  // h->host_err was filled by an async copy already synchronised by the caller
-  (void)s;
-  const DevError e = *h->host_err;
+rlo_status device_error_status(const DevError& e) {
   if (e.code == DE_NONE) return RLO_OK;
   switch (e.code) {
     case DE_OOV_LOGPROB:  // policy.cpp:224-225
@@ -431,6 +412,12 @@ rlo_status collect_device_error(rlo_handle* h, cudaStream_t s) {
       return fail(RLO_ERR_INPUT, "sample batch: response length of sample '" + std::to_string(e.value) +
                                      "' is outside [0, T]");
   }
+}
+
+rlo_status collect_device_error(rlo_handle* h, cudaStream_t s) {
+  // h->host_err was filled by an async copy already synchronised by the caller
+  (void)s;
+  return device_error_status(*h->host_err);
 }
 
 }  // namespace
@@ -725,6 +712,46 @@ rlo_status rlo_merge_gradients(rlo_handle* h, const rlo_train_config* cfg, rlo_s
     std::memcpy(parts[static_cast<size_t>(r)].v, h->host_gathered + r * RLO_NPARTIAL, sizeof(double) * RLO_NPARTIAL);
   if (out_partials) *out_partials = parts[static_cast<size_t>(h->comm ? h->rank : 0)];
   return rlo_merge_partials(parts.data(), world, cfg, out);
+}
+
+rlo_status rlo_merge_gradients_async(rlo_handle* h, const rlo_train_config* cfg, rlo_step_result* out,
+                                     void* stream) {
+  if (!h) return fail(RLO_ERR_INPUT, "merge_gradients: null handle");
+  RLO_TRY(rlo_train_config_validate(cfg));
+  if (!out) return fail(RLO_ERR_INPUT, "merge_gradients_async: out required");
+  DeviceGuard g(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int32_t nseq = h->acc_nseq;
+  if (nseq > 0) {
+    RLO_CUDA(launch_batch_reduce(h->recs.p, nseq, cfg->group_size, h->partials.p, s));
+  } else {
+    RLO_CUDA(cudaMemsetAsync(h->partials.p, 0, sizeof(double) * RLO_NPARTIAL, s));
+  }
+  const double* parts = h->partials.p;
+  int world = 1;
+  if (h->comm) {  // all-gather of the per-rank partials, merged in rank order on the device
+    RLO_NCCL(nccl_api().AllGather(h->partials.p, h->gathered.p, RLO_NPARTIAL, ncclFloat64, h->comm, s));
+    parts = h->gathered.p;
+    world = h->world;
+  }
+  RLO_CUDA(launch_merge_finalize(parts, world, cfg->loss_agg, h->err.p, out, s));
+  if (nseq > 0) RLO_CUDA(cudaMemsetAsync(h->recs.p, 0, sizeof(SeqRec) * static_cast<size_t>(nseq), s));
+  h->acc_nseq = 0;
+  return RLO_OK;
+}
+
+rlo_status rlo_step_result_check(const rlo_step_result* r) {
+  if (!r) return fail(RLO_ERR_INPUT, "step_result_check: null result");
+  switch (r->reason) {
+    case 0: return RLO_OK;
+    case 1: return fail(RLO_ERR_TRAINING, "merge_gradients: batch contains no loss-participating tokens");
+    case 2: return fail(RLO_ERR_TRAINING, "training step aborted: non-finite gradient");
+    case 3: return fail(RLO_ERR_TRAINING, "training step aborted: non-finite loss");
+    default: {
+      DevError e{r->dev_error, r->dev_error_value};
+      return device_error_status(e);
+    }
+  }
 }
 
 rlo_status rlo_rank_partials(rlo_handle* h, const rlo_train_config* cfg, rlo_partials* out, void* stream) {

@@ -69,6 +69,39 @@ RLO_HOST_DEVICE inline int whiten_combine(const double* stats_all, int world, do
   return 1;
 }
 
+// merge_gradients normalisation (policy.cpp:421-450) of rank-ordered
+// partials parts[r*RLO_NPARTIAL + k]: returns 0, or the reason the reference
+// aborts (1 no tokens, 2 non-finite gradient, 3 non-finite loss).  Shared by
+// the host merge and the device finalize kernel (graph-capturable step).
+RLO_HOST_DEVICE inline int32_t merge_stats(const double* parts, int32_t world, int32_t agg, rlo_stats* st) {
+  double s[RLO_NPARTIAL];
+  for (int k = 0; k < RLO_NPARTIAL; ++k) s[k] = 0.0;
+  for (int32_t r = 0; r < world; ++r)
+    for (int k = 0; k < RLO_NPARTIAL; ++k) s[k] += parts[r * RLO_NPARTIAL + k];
+  if (s[RLO_P_TOKENS] == 0.0) return 1;
+  if (s[RLO_P_NONFINITE_GRAD] > 0.0) return 2;
+  const double inv = 1.0 / s[RLO_P_TOKENS];
+  rlo_stats o;
+  if (agg == RLO_AGG_SEQ_MEAN_TOKEN_MEAN)
+    o.loss = s[RLO_P_SEQ_MEAN_SUM] * (1.0 / s[RLO_P_SEQS]);
+  else if (agg == RLO_AGG_SEQ_MEAN_TOKEN_SUM)
+    o.loss = s[RLO_P_LOSS_SUM] * (1.0 / s[RLO_P_SEQS]);
+  else if (agg == RLO_AGG_GROUP_MEAN)
+    o.loss = s[RLO_P_GROUP_MEAN_SUM] * (1.0 / s[RLO_P_GROUPS]);
+  else
+    o.loss = s[RLO_P_LOSS_SUM] * inv;
+  o.mean_ratio = s[RLO_P_RATIO_SUM] * inv;
+  o.clip_fraction = s[RLO_P_CLIPPED] * inv;
+  o.mean_kl = s[RLO_P_KL_SUM] * inv;
+  o.tokens = static_cast<uint64_t>(s[RLO_P_TOKENS]);
+  o.mean_entropy = s[RLO_P_ENTROPY_SUM] * inv;
+  o.dual_clip_fraction = s[RLO_P_DUAL_CLIPPED] * inv;
+  o.seqs = static_cast<uint64_t>(s[RLO_P_SEQS]);
+  o.groups = static_cast<uint64_t>(s[RLO_P_GROUPS]);
+  *st = o;
+  return isfinite(o.loss) ? 0 : 3;
+}
+
 struct VocabArgs {
   const void* logits[3];
   int64_t stride[3];
@@ -138,6 +171,8 @@ cudaError_t launch_seq_reduce(int32_t B, int32_t T, int32_t seq_offset, const in
                               const uint8_t* mask, const float* s_loss, const float* s_ratio,
                               const float* s_kl, const float* s_ent, const uint8_t* s_flags, SeqRec* recs,
                               cudaStream_t s);
+cudaError_t launch_merge_finalize(const double* parts, int32_t world, int32_t agg, DevError* err,
+                                  rlo_step_result* out, cudaStream_t s);
 cudaError_t launch_batch_reduce(const SeqRec* recs, int32_t nseq, int32_t G, double* partials,
                                 cudaStream_t s);
 cudaError_t launch_advantages(const AdvArgs& a, cudaStream_t s);

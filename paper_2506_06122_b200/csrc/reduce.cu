@@ -115,7 +115,30 @@ __global__ void __launch_bounds__(kBR) batch_reduce_kernel(const SeqRec* __restr
   }
 }
 
+// One thread: rank-ordered merge of the all-gathered partials into the step
+// result (rlo_merge_gradients_async), plus the device error slot, which it
+// then clears for the next step.
+__global__ void merge_finalize_kernel(const double* __restrict__ parts, int world, int agg, DevError* err,
+                                      rlo_step_result* out) {
+  rlo_step_result r;
+  r.stats = rlo_stats{};
+  r.dev_error = err->code;
+  r.dev_error_value = err->value;
+  r.reason = r.dev_error ? 4 : merge_stats(parts, world, agg, &r.stats);
+  r.status = r.reason == 0 ? RLO_OK : r.reason == 4 ? RLO_ERR_INPUT : RLO_ERR_TRAINING;
+  *out = r;
+  err->code = 0;
+  err->value = 0;
+}
+
 }  // namespace
+
+cudaError_t launch_merge_finalize(const double* parts, int32_t world, int32_t agg, DevError* err,
+                                  rlo_step_result* out, cudaStream_t s) {
+  merge_finalize_kernel<<<1, 1, 0, s>>>(parts, world, agg, err, out);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_seq_reduce(int32_t B, int32_t T, int32_t seq_offset, const int32_t* lengths,
                               const uint8_t* mask, const float* s_loss, const float* s_ratio,

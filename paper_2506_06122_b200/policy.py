@@ -309,6 +309,27 @@ class Objective:
         stats = UpdateStats.from_c(st)
         return (stats, np.array(part.v[:])) if with_partials else stats
 
+    def merge_gradients_async(self, cfg: TrainConfig, out=None, stream=None):
+        """merge_gradients with no host synchronisation (CUDA-graph capturable):
+        the merged UpdateStats and the error status land in `out`, a device
+        uint8 tensor of sizeof(rlo_step_result) bytes (allocated when None).
+        Read it with step_result()."""
+        torch = _torch()
+        if out is None:
+            out = torch.zeros(C.sizeof(_abi.rlo_step_result), dtype=torch.uint8, device=self.device)
+        check(_abi.lib().rlo_merge_gradients_async(self._h, C.byref(cfg.to_c()), C.c_void_p(out.data_ptr()),
+                                                   _stream(stream, self.device)))
+        return out
+
+    @staticmethod
+    def step_result(buf) -> UpdateStats:
+        """UpdateStats of a merge_gradients_async result (copies it to the host);
+        raises what the synchronous merge_gradients would have raised."""
+        raw = bytes(buf.cpu().numpy().tobytes())
+        r = _abi.rlo_step_result.from_buffer_copy(raw)
+        check(_abi.lib().rlo_step_result_check(C.byref(r)))
+        return UpdateStats.from_c(r.stats)
+
     # -- next rows: backward epilogue, critic ----------------------------------
     def loss_weights(self, cfg: TrainConfig, lengths, stats: "UpdateStats", T, mask=None, stream=None):
         """d(L)/d(loss_t) per token under cfg.loss_agg with the merged counts."""

@@ -517,3 +517,55 @@ def test_aggregation_and_dual_clip_identities_on_gpu(env):
                              ref_logprobs=dev(torch, _arr(c["ref"]).reshape(B, T)))
             st = obj.merge_gradients(cfg)
             assert close(st.loss, c["ref_stats"]["loss"], tol=2e-5), (extra, st.loss, c["ref_stats"]["loss"])
+
+
+def test_whole_step_in_a_cuda_graph(env):
+    """compute_advantages -> ppo_gradient -> merge_gradients_async captured in
+    a CUDA graph and replayed: the same UpdateStats as the synchronous step,
+    fresh inputs picked up on replay, errors reported through the result."""
+    torch, rlo, obj = env
+    B, T, V, G = 8, 32, 4096, 4
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    x = [torch.randn(B * T, V, device="cuda", generator=gen) * 2 for _ in range(3)]
+    K = torch.randint(0, V, (B, T), device="cuda", dtype=torch.int32, generator=gen)
+    L = torch.tensor([T, T - 3, T, 5, T, 1, T, 9], dtype=torch.int32, device="cuda")
+    M = torch.ones(B, T, dtype=torch.uint8, device="cuda")
+    R = torch.rand(B, device="cuda", generator=gen)
+    adv = torch.empty(B, T, device="cuda")
+    res = torch.zeros(88, dtype=torch.uint8, device="cuda")
+    cfg = rlo.TrainConfig(adv_estimator="grpo", group_size=G, kl_coef=0.01, kl_estimator="k3")
+
+    def sync_step():
+        obj.compute_advantages(cfg, L, T=T, mask=M, scalar_rewards=R, out=adv)
+        obj.ppo_gradient(cfg, K, L, x[0], adv, mask=M, old_logits=x[1], ref_logits=x[2], outputs=())
+        return obj.merge_gradients(cfg)
+
+    def async_step():
+        obj.compute_advantages(cfg, L, T=T, mask=M, scalar_rewards=R, out=adv)
+        obj.ppo_gradient(cfg, K, L, x[0], adv, mask=M, old_logits=x[1], ref_logits=x[2], outputs=())
+        obj.merge_gradients_async(cfg, out=res)
+
+    want = sync_step()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        async_step()  # warm-up: every workspace buffer is sized before capture
+    torch.cuda.synchronize()
+    assert rlo.Objective.step_result(res) == want
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        async_step()
+    res.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert rlo.Objective.step_result(res) == want
+    R.copy_(torch.rand(B, device="cuda", generator=gen))  # new rewards, same buffers
+    g.replay()
+    torch.cuda.synchronize()
+    got = rlo.Objective.step_result(res)
+    assert got == sync_step() and got != want
+    M.zero_()  # no participating token: the reference's TrainingError, through the result
+    g.replay()
+    torch.cuda.synchronize()
+    with pytest.raises(rlo.TrainingError, match="no loss-participating tokens"):
+        rlo.Objective.step_result(res)
