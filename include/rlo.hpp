@@ -132,6 +132,17 @@ class Objective {
     check(rlo_merge_gradients(h_, &cfg, &st, mine, stream));
     return st;
   }
+  // merge_gradients without host synchronisation (CUDA-graph capturable):
+  // `out` is device (or host-mapped) memory; read it with step_result().
+  void merge_gradients_async(const TrainConfig& cfg, rlo_step_result* out, void* stream = nullptr) {
+    check(rlo_merge_gradients_async(h_, &cfg, out, stream));
+  }
+  // UpdateStats of a host copy of a merge_gradients_async result; throws what
+  // the synchronous merge_gradients would have thrown.
+  static UpdateStats step_result(const rlo_step_result& host_copy) {
+    check(rlo_step_result_check(&host_copy));
+    return host_copy.stats;
+  }
   Partials rank_partials(const TrainConfig& cfg, void* stream = nullptr) {
     Partials p{};
     check(rlo_rank_partials(h_, &cfg, &p, stream));
