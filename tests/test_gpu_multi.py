@@ -26,4 +26,4 @@ def test_data_parallel_equals_single_gpu(world):
                         os.path.join(ROOT, "tools", "dp_check.py")], capture_output=True, text=True, timeout=600)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0
-    assert r.stdout.count("PASS") == 8 and "FAIL" not in r.stdout
+    assert r.stdout.count("PASS") == 9 and "FAIL" not in r.stdout

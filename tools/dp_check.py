@@ -122,6 +122,27 @@ def main():
               f"dlogits max err {g_err:.2e}, loss {st.loss:.12f} vs {st1.loss:.12f}", flush=True)
         fails += not ok
         single.close()
+    # device-side (graph-capturable) merge over NCCL == the synchronous merge
+    cfg = cfgs["grpo+whiten+group-mean"]
+    Ls, Ms = d(lengths[b0:b0 + n]), d(mask[b0:b0 + n])
+
+    def body():
+        adv = obj.compute_advantages(cfg, Ls, T=T, mask=Ms, scalar_rewards=d(rs[b0:b0 + n]))
+        obj.ppo_gradient(cfg, toks[b0:b0 + n].contiguous(), Ls, full[0][rows], adv, mask=Ms,
+                         old_logits=full[1][rows], ref_logits=full[2][rows], outputs=())
+    body()
+    st_sync = obj.merge_gradients(cfg)
+    body()
+    res = obj.merge_gradients_async(cfg)
+    st_async = rlo.Objective.step_result(res)
+    ok = st_sync == st_async
+    okt = torch.tensor([int(ok)], device=dev)
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        good = bool(okt.item())
+        print(f"{'PASS' if good else 'FAIL'} dp{world} async (device-side) merge == synchronous merge: "
+              f"loss {st_async.loss:.12f}", flush=True)
+        fails += not good
     # ModelUpdateGroup: bucketed broadcast, destinations bit-identical for every
     # bucket size (test_policy_workers.cpp:100-130's sync_params property)
     n_params = 1_000_003
