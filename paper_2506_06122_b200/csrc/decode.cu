@@ -60,8 +60,11 @@ __device__ __forceinline__ float logit<__nv_bfloat16>(const __nv_bfloat16* p, in
 // ~20 of the library exp(); t < -708 is clamped (3e-308, below every sum it
 // enters).
 constexpr int kExpTab = 256;
-__device__ __forceinline__ double exp_neg(double t, const double* __restrict__ tab) {
-  t = fmax(t, -708.0);  // branch-free: exp(-708) = 3e-308 stands in for 0 (and for -inf logits)
+// Unclamped core: t must be >= -708 (the callers clamp the fp32 logit to
+// m - 700*T, one FMNMX, so -inf logits weigh exp(-700/T) ~ 1e-304 instead of 0
+// — below any sum they enter, as with the clamp).  2^k is added to the high
+// word only.
+__device__ __forceinline__ double exp_neg_core(double t, const double* __restrict__ tab) {
   constexpr double kMagic = 6755399441055744.0;   // 1.5 * 2^52: round to integer
   constexpr double k256Ln2 = 369.32993046757462;  // 256 / ln 2
   constexpr double kLn2o256Hi = 0x1.62e42fefa0000p-9, kLn2o256Lo = 0x1.cf79abc9e3b3ap-48;
@@ -75,7 +78,10 @@ __device__ __forceinline__ double exp_neg(double t, const double* __restrict__ t
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
   const double v = tab[n & (kExpTab - 1)] * p;
-  return __longlong_as_double(__double_as_longlong(v) + ((long long)(n >> 8) << 52));
+  return __hiloint2double(__double2hiint(v) + ((n >> 8) << 20), __double2loint(v));
+}
+__device__ __forceinline__ double exp_neg(double t, const double* __restrict__ tab) {
+  return exp_neg_core(fmax(t, -708.0), tab);  // branch-free: exp(-708) = 3e-308 stands in for 0
 }
 
 template <typename ET>
@@ -142,6 +148,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   for (int j = threadIdx.x; j < kExpTab; j += blockDim.x) tab[j] = exp2((double)j / kExpTab);
   __syncthreads();
   const double inv_t = 1.0 / temp;
+  const float ftemp = (float)temp;
   const bool unit_t = temp == 1.0;
   const int W = ((V + kDecWarps - 1) / kDecWarps + 32 * E - 1) / (32 * E) * (32 * E);
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(logits) & 15u) == 0) && (((stride * (int64_t)sizeof(ET)) & 15) == 0);
@@ -149,7 +156,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     const ET* z = logits + (int64_t)row * stride;
     const int v0 = warp * W, v1 = min(V, v0 + W);
     // pass 1
-    float m = -INFINITY, mL = kNegInit * kL2E, su = 0.f;
+    float m = -INFINITY, mL = kNegInit * kL2E, su = 0.f, lo = -INFINITY;
     double st = 0.0;
     for (int b = v0 + lane * E; b < v1; b += 32 * E) {
       float x[8];
@@ -160,6 +167,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
       if (cm > m) {
         if (m != -INFINITY) st *= exp_neg(unit_t ? (double)m - cm : ((double)m - cm) * inv_t, tab);
         m = cm;
+        lo = m - 700.f * ftemp;  // clamp bound for exp_neg_core
         const float nmL = __fmul_rn(cm, kL2E);
         su *= ex2(mL - nmL);
         mL = nmL;
@@ -169,8 +177,8 @@ __global__ void __launch_bounds__(kDecWarps * 32)
       float q[8];
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const double d = (double)x[e] - (double)m;
-        w[e] = exp_neg(unit_t ? d : d * inv_t, tab);
+        const double d = (double)fmaxf(x[e], lo) - (double)m;
+        w[e] = exp_neg_core(unit_t ? d : d * inv_t, tab);
         q[e] = ex2(fmaf(x[e], kL2E, -mL));  // -inf -> ex2(-inf) = 0
       }
 #pragma unroll
@@ -238,6 +246,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
       // pass 2a: the 8 warps split the crossing warp's range into 8 sub-ranges
       // and sum their weights (relative to the row max) in parallel
       const double M = s_M;
+      const float loM = s_M - 700.f * ftemp;
       const int a0 = jw * W, a1 = min(V, a0 + W);
       const int W2 = ((W + kDecWarps - 1) / kDecWarps + 32 * E - 1) / (32 * E) * (32 * E);
       {
@@ -249,8 +258,8 @@ __global__ void __launch_bounds__(kDecWarps * 32)
           load_e<ET>(z, b, c1, vec_ok, x);
 #pragma unroll
           for (int e = 0; e < E; ++e) {
-            const double d = (double)x[e] - M;
-            w[e] = b + e < c1 ? exp_neg(unit_t ? d : d * inv_t, tab) : 0.0;
+            const double d = (double)fmaxf(x[e], loM) - M;
+            w[e] = b + e < c1 ? exp_neg_core(unit_t ? d : d * inv_t, tab) : 0.0;
           }
 #pragma unroll
           for (int h = E / 2; h > 0; h >>= 1) {
@@ -292,8 +301,8 @@ __global__ void __launch_bounds__(kDecWarps * 32)
           load_e<ET>(z, b, c1, vec_ok, x);
 #pragma unroll
           for (int e = 0; e < E; ++e) {
-            const double d = (double)x[e] - M;
-            w[e] = b + e < c1 ? exp_neg(unit_t ? d : d * inv_t, tab) : 0.0;
+            const double d = (double)fmaxf(x[e], loM) - M;
+            w[e] = b + e < c1 ? exp_neg_core(unit_t ? d : d * inv_t, tab) : 0.0;
             ls += w[e];
           }
           double incl = ls;
