@@ -85,6 +85,28 @@ def _big_jsonl(n, T, seed=5):
     return "\n".join(lines)
 
 
+def bench_advantages(obj):
+    """compute_advantages at long-CoT shapes (the O(N) part of the path)."""
+    for est, B, T in (("gae", 256, 16384), ("gae", 2048, 2048), ("reinforce", 256, 16384), ("grpo", 2048, 2048)):
+        g = torch.Generator(device="cuda").manual_seed(1)
+        L = torch.full((B,), T, dtype=torch.int32, device="cuda")
+        kw = {}
+        if est == "grpo":
+            kw["scalar_rewards"] = torch.rand(B, device="cuda", generator=g)
+        else:
+            kw["rewards"] = torch.randn(B, T, device="cuda", generator=g) * 0.1
+        if est == "gae":
+            kw["values"] = torch.randn(B, T, device="cuda", generator=g) * 0.5
+        cfg = rlo.TrainConfig(adv_estimator=est, group_size=16 if est == "grpo" else 1, whiten_advantages=True,
+                              gamma=0.99, lambd=0.95)
+        out = torch.empty(B, T, device="cuda")
+        ms = timed(lambda: obj.compute_advantages(cfg, L, T=T, out=out, **kw))
+        byts = B * T * (4 + 4 + (4 if est == "gae" else 0) + 8 + 8)  # rewards, adv, values, fp64 scratch w+r
+        print(json.dumps({"row": "advantages", "estimator": est, "B": B, "T": T, "ms": ms,
+                          "tokens_per_s": B * T / ms * 1e3, "gbs": byts / ms / 1e6,
+                          "note": "whitened (global stats), fp64 scan"}), flush=True)
+
+
 def bench_jsonl():
     import oracle as O
     cases = []
@@ -139,7 +161,7 @@ def bench_broadcast():
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="decode,value,jsonl")
+    ap.add_argument("--only", default="decode,value,advantages,jsonl")
     args = ap.parse_args()
     rows = args.only.split(",")
     if "broadcast" in rows:
@@ -150,6 +172,8 @@ def main():
         bench_decode(obj)
     if "value" in rows:
         bench_value(obj)
+    if "advantages" in rows:
+        bench_advantages(obj)
     if "jsonl" in rows:
         bench_jsonl()
 
