@@ -39,7 +39,7 @@ extern "C" {
 #pragma GCC visibility push(default) /* the library is built -fvisibility=hidden; export exactly this header */
 #endif
 
-#define RLO_ABI_VERSION 3
+#define RLO_ABI_VERSION 4
 
 /* Status codes — reference exception taxonomy (include/rollmini/errors.hpp). */
 typedef enum rlo_status {
@@ -129,6 +129,7 @@ typedef struct rlo_token_out {
   float* dlogp;     /* d(loss_t)/d(logp_t), policy.cpp:372-374 */
   float* loss;      /* per-token loss contribution (0 for non-participating tokens) */
   float* lse;       /* actor log-sum-exp of the row (input of rlo_logits_backward) */
+  double* lse64;    /* the same in fp64 (input of rlo_logits_backward64: exact at any logit offset) */
 } rlo_token_out;
 
 /* Critic value-loss statistics (value_gradient, policy.cpp:474-540). */
@@ -349,12 +350,20 @@ rlo_status rlo_batch_counts(rlo_handle* h, const rlo_train_config* cfg, const rl
  * other rows of `grad` are zeroed (with packed logits, rlo_logits.seq_start,
  * gradient rows follow the same layout and only existing rows are written).
  * The lse is fp32, so p carries its rounding (relative <= ulp(lse)/2: 4e-6 at
- * |lse| < 64); the fused pass below has no such term.  grad has grad_dtype (rlo_dtype) and
+ * |lse| < 64); rlo_logits_backward64 (fp64 lse) and the fused pass have no
+ * such term.  grad has grad_dtype (rlo_dtype) and
  * grad_row_stride; lse / dlogp / weight are [B*T] (rlo_token_out.lse,
  * rlo_token_out.dlogp, rlo_loss_weights). */
 rlo_status rlo_logits_backward(rlo_handle* h, const rlo_batch* batch, const rlo_logits* logits, const float* lse,
                                const float* dlogp, const float* weight, void* grad, int32_t grad_dtype,
                                int64_t grad_row_stride, void* stream);
+
+/* rlo_logits_backward with the fp64 lse (rlo_token_out.lse64): the softmax is
+ * rebuilt as 2^(z*log2e - (lse*log2e)_hi - (lse*log2e)_lo), so the fp32
+ * rounding of the lse drops out (relative error ~1e-7 at any logit offset). */
+rlo_status rlo_logits_backward64(rlo_handle* h, const rlo_batch* batch, const rlo_logits* logits, const double* lse64,
+                                 const float* dlogp, const float* weight, void* grad, int32_t grad_dtype,
+                                 int64_t grad_row_stride, void* stream);
 
 /* Fused update pass: rlo_ppo_gradient (same inputs, outputs, accumulation and
  * errors) and the actor backward epilogue in ONE read of the actor logits

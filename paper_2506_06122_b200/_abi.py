@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # RLO_LIB overrides the in-tree library (A/B builds of the same sources in kernel experiments).
 LIB_PATH = os.environ.get("RLO_LIB") or os.path.join(HERE, "lib", "librlo.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "rlo.h")
-ABI_VERSION = 3  # include/rlo.h RLO_ABI_VERSION: the struct layouts below
+ABI_VERSION = 4  # include/rlo.h RLO_ABI_VERSION: the struct layouts below
 
 RLO_OK, RLO_ERR_INPUT, RLO_ERR_CONFIG, RLO_ERR_TRAINING, RLO_ERR_CUDA, RLO_ERR_NCCL, RLO_ERR_DISPATCH = range(7)
 DTYPE_F32, DTYPE_BF16 = 0, 1
@@ -46,7 +46,8 @@ class rlo_logits(C.Structure):
 
 class rlo_token_out(C.Structure):
     _fields_ = [("logp", C.c_void_p), ("old_logp", C.c_void_p), ("ref_logp", C.c_void_p),
-                ("entropy", C.c_void_p), ("dlogp", C.c_void_p), ("loss", C.c_void_p), ("lse", C.c_void_p)]
+                ("entropy", C.c_void_p), ("dlogp", C.c_void_p), ("loss", C.c_void_p), ("lse", C.c_void_p),
+                ("lse64", C.c_void_p)]
 
 
 class rlo_stats(C.Structure):
@@ -132,6 +133,7 @@ def lib() -> C.CDLL:
         "rlo_sync": ([vp, vp], C.c_int),
         "rlo_loss_weights": ([vp, P(rlo_train_config), P(rlo_batch), P(rlo_stats), vp, vp], C.c_int),
         "rlo_logits_backward": ([vp, P(rlo_batch), P(rlo_logits), vp, vp, vp, vp, i32, i64, vp], C.c_int),
+        "rlo_logits_backward64": ([vp, P(rlo_batch), P(rlo_logits), vp, vp, vp, vp, i32, i64, vp], C.c_int),
         "rlo_batch_counts": ([vp, P(rlo_train_config), P(rlo_batch), P(rlo_stats), vp], C.c_int),
         "rlo_ppo_gradient_fused": ([vp, P(rlo_train_config), P(rlo_batch), P(rlo_logits), P(rlo_logits),
                                     P(rlo_logits), vp, vp, vp, vp, vp, i32, i64, P(rlo_token_out), vp], C.c_int),

@@ -159,7 +159,8 @@ struct rlo_handle {
   int32_t acc_nseq = 0;
   // per-token scratch of the loss pass
   DevBuf<float> s_loss, s_ratio, s_kl, s_ent;
-  DevBuf<float> s_lse, s_dlogp;  // two-pass fallback of the fused update pass
+  DevBuf<float> s_dlogp;  // two-pass fallback of the fused update pass
+  DevBuf<double> s_lse64;
   DevBuf<uint8_t> s_flags;
   // whitening
   DevBuf<WStat> wstat;
@@ -606,6 +607,7 @@ rlo_status ppo_setup(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch
     a.o_dlogp = out->dlogp;
     a.o_loss = out->loss;
     a.o_lse = out->lse;
+    a.o_lse64 = out->lse64;
   }
   a.s_loss = h->s_loss.p;
   a.s_ratio = h->s_ratio.p;
@@ -665,15 +667,14 @@ rlo_status rlo_ppo_gradient_fused(rlo_handle* h, const rlo_train_config* cfg, co
     // memory): the two-pass form, loss pass then backward epilogue
     cudaGetLastError();
     const int64_t N = (int64_t)B * T;
-    RLO_CUDA(h->s_lse.ensure(N));
+    RLO_CUDA(h->s_lse64.ensure(N));
     RLO_CUDA(h->s_dlogp.ensure(N));
-    if (!a.o_lse) a.o_lse = h->s_lse.p;
+    if (!a.o_lse64) a.o_lse64 = h->s_lse64.p;
     if (!a.o_dlogp) a.o_dlogp = h->s_dlogp.p;
     RLO_CUDA(launch_vocab_loss(a, h->num_sms, s));
     RLO_CUDA(launch_logits_backward(actor->data, actor->dtype, actor->row_stride, actor->seq_start, actor->V, B, T,
-                                    batch->lengths,
-                                    batch->tokens, a.o_lse, a.o_dlogp, weight, grad, grad_dtype, grad_row_stride,
-                                    h->num_sms, s));
+                                    batch->lengths, batch->tokens, nullptr, a.o_lse64, a.o_dlogp, weight, grad,
+                                    grad_dtype, grad_row_stride, h->num_sms, s));
   }
   RLO_CUDA(launch_seq_reduce(B, T, batch->seq_offset, batch->lengths, batch->mask, h->s_loss.p, h->s_ratio.p,
                              h->s_kl.p, h->s_ent.p, h->s_flags.p, h->recs.p, s));
@@ -888,23 +889,39 @@ rlo_status rlo_loss_weights(rlo_handle* h, const rlo_train_config* cfg, const rl
   return RLO_OK;
 }
 
-rlo_status rlo_logits_backward(rlo_handle* h, const rlo_batch* batch, const rlo_logits* logits, const float* lse,
-                               const float* dlogp, const float* weight, void* grad, int32_t grad_dtype,
-                               int64_t grad_row_stride, void* stream) {
+namespace {
+rlo_status logits_backward_impl(rlo_handle* h, const rlo_batch* batch, const rlo_logits* logits, const float* lse,
+                                const double* lse64, const float* dlogp, const float* weight, void* grad,
+                                int32_t grad_dtype, int64_t grad_row_stride, void* stream) {
   if (!h) return fail(RLO_ERR_INPUT, "logits_backward: null handle");
   RLO_TRY(check_batch(batch, "logits_backward", true));
   RLO_TRY(check_logits(logits, "logits_backward", "actor"));
   if ((int64_t)batch->B * batch->T == 0) return RLO_OK;
-  if (!lse || !dlogp || !weight || !grad) return fail(RLO_ERR_INPUT, "logits_backward: lse, dlogp, weight, grad required");
+  if ((!lse && !lse64) || !dlogp || !weight || !grad)
+    return fail(RLO_ERR_INPUT, "logits_backward: lse, dlogp, weight, grad required");
   if (grad_dtype != RLO_DTYPE_F32 && grad_dtype != RLO_DTYPE_BF16)
     return fail(RLO_ERR_INPUT, "logits_backward: unsupported grad dtype");
   if (grad_row_stride < logits->V) return fail(RLO_ERR_INPUT, "logits_backward: grad row stride < V");
   DeviceGuard g(h->device);
   RLO_CUDA(launch_logits_backward(logits->data, logits->dtype, logits->row_stride, logits->seq_start, logits->V,
-                                  batch->B, batch->T,
-                                  batch->lengths, batch->tokens, lse, dlogp, weight, grad, grad_dtype, grad_row_stride,
-                                  h->num_sms, static_cast<cudaStream_t>(stream)));
+                                  batch->B, batch->T, batch->lengths, batch->tokens, lse, lse64, dlogp, weight, grad,
+                                  grad_dtype, grad_row_stride, h->num_sms, static_cast<cudaStream_t>(stream)));
   return RLO_OK;
+}
+}  // namespace
+
+rlo_status rlo_logits_backward(rlo_handle* h, const rlo_batch* batch, const rlo_logits* logits, const float* lse,
+                               const float* dlogp, const float* weight, void* grad, int32_t grad_dtype,
+                               int64_t grad_row_stride, void* stream) {
+  return logits_backward_impl(h, batch, logits, lse, nullptr, dlogp, weight, grad, grad_dtype, grad_row_stride,
+                              stream);
+}
+
+rlo_status rlo_logits_backward64(rlo_handle* h, const rlo_batch* batch, const rlo_logits* logits,
+                                 const double* lse64, const float* dlogp, const float* weight, void* grad,
+                                 int32_t grad_dtype, int64_t grad_row_stride, void* stream) {
+  return logits_backward_impl(h, batch, logits, nullptr, lse64, dlogp, weight, grad, grad_dtype, grad_row_stride,
+                              stream);
 }
 
 rlo_status rlo_value_loss(rlo_handle* h, const rlo_batch* batch, const float* values, const float* old_values,

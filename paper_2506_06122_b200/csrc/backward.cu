@@ -93,6 +93,7 @@ struct BwArgs {
   const int32_t* lengths;
   const int32_t* tokens;
   const float* lse;
+  const double* lse64;  // when set, used instead of lse (hi/lo split in log2 units)
   const float* dlogp;
   const float* weight;
   void* grad;
@@ -152,10 +153,18 @@ __global__ void __launch_bounds__(kBwThreads) logits_backward_kernel(const BwArg
       continue;
     }
     const int tok = __ldg(a.tokens + row);
-    const float nl = -__ldg(a.lse + row) * kL2E;
+    // -(lse * log2e) as hi + lo floats: exact for the fp64 lse, the fp32 lse's own rounding otherwise
+    float nl, nlo = 0.f;
+    if (a.lse64) {
+      const double L = __ldg(a.lse64 + row) * (double)kL2E;
+      nl = (float)-L;
+      nlo = (float)(-L - (double)nl);
+    } else {
+      nl = -__ldg(a.lse + row) * kL2E;
+    }
     const float ms = -scale;
     auto one = [&](int v) {
-      float o = ms * ex2(fmaf(In<ET>::one(z + v), kL2E, nl));
+      float o = ms * ex2(fmaf(In<ET>::one(z + v), kL2E, nl) + nlo);
       if (v == tok) o += scale;
       Out<GT>::one(g + v, o);
     };
@@ -164,7 +173,7 @@ __global__ void __launch_bounds__(kBwThreads) logits_backward_kernel(const BwArg
       float x[8], o[8];
       In<ET>::load(zb + (int64_t)i * N, x);
 #pragma unroll
-      for (int k = 0; k < N; ++k) o[k] = ms * ex2(fmaf(x[k], kL2E, nl));  // -w*dlp*p_v
+      for (int k = 0; k < N; ++k) o[k] = ms * ex2(fmaf(x[k], kL2E, nl) + nlo);  // -w*dlp*p_v
       const int d = tok - head - i * N;
       if (d >= 0 && d < N) {
 #pragma unroll
@@ -216,10 +225,10 @@ cudaError_t launch_batch_counts(int32_t B, int32_t T, int32_t G, const int32_t* 
 
 cudaError_t launch_logits_backward(const void* logits, int32_t dtype, int64_t stride, const int64_t* seq_start,
                                    int32_t V, int32_t B, int32_t T,
-                                   const int32_t* lengths, const int32_t* tokens, const float* lse, const float* dlogp,
-                                   const float* weight, void* grad, int32_t gdtype, int64_t gstride, int num_sms,
-                                   cudaStream_t s) {
-  const BwArgs a{logits, stride, seq_start, V, B, T, lengths, tokens, lse, dlogp, weight, grad, gstride};
+                                   const int32_t* lengths, const int32_t* tokens, const float* lse,
+                                   const double* lse64, const float* dlogp, const float* weight, void* grad,
+                                   int32_t gdtype, int64_t gstride, int num_sms, cudaStream_t s) {
+  const BwArgs a{logits, stride, seq_start, V, B, T, lengths, tokens, lse, lse64, dlogp, weight, grad, gstride};
   if (dtype == RLO_DTYPE_BF16)
     return gdtype == RLO_DTYPE_BF16 ? launch_bw<__nv_bfloat16, __nv_bfloat16>(a, num_sms, s)
                                     : launch_bw<__nv_bfloat16, float>(a, num_sms, s);

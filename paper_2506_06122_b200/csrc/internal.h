@@ -132,6 +132,7 @@ struct VocabArgs {
   float* o_dlogp;
   float* o_loss;
   float* o_lse;
+  double* o_lse64;
   // scratch consumed by the per-sequence reduction
   float* s_loss;
   float* s_ratio;
@@ -187,7 +188,8 @@ cudaError_t launch_batch_counts(int32_t B, int32_t T, int32_t G, const int32_t* 
                                 float* counts, double* out4, cudaStream_t s);
 cudaError_t launch_logits_backward(const void* logits, int32_t dtype, int64_t stride, const int64_t* seq_start,
                                    int32_t V, int32_t B, int32_t T,
-                                   const int32_t* lengths, const int32_t* tokens, const float* lse, const float* dlogp,
+                                   const int32_t* lengths, const int32_t* tokens, const float* lse,
+                                   const double* lse64, const float* dlogp,
                                    const float* weight, void* grad, int32_t gdtype, int64_t gstride, int num_sms,
                                    cudaStream_t s);
 cudaError_t launch_value_loss(int32_t B, int32_t T, const int32_t* lengths, const uint8_t* mask, const float* values,

@@ -381,6 +381,7 @@ __device__ inline double loss_epilogue(const VocabArgs& a, int64_t row, double l
   if (a.o_dlogp) a.o_dlogp[row] = (float)dlp;
   if (a.o_loss) a.o_loss[row] = (float)loss;
   if (a.o_lse) a.o_lse[row] = (float)lse;
+  if (a.o_lse64) a.o_lse64[row] = lse;
   return dlp;
 }
 
@@ -439,6 +440,7 @@ __device__ __forceinline__ void write_inactive(const VocabArgs& a, int64_t row) 
     if (a.o_dlogp) a.o_dlogp[row] = 0.f;
     if (a.o_loss) a.o_loss[row] = 0.f;
     if (a.o_lse) a.o_lse[row] = 0.f;
+    if (a.o_lse64) a.o_lse64[row] = 0.0;
   }
 }
 

@@ -287,9 +287,10 @@ class Objective:
         _check_dev(mask, torch.uint8, "mask")
         for t, n in ((advantages, "advantages"), (old_logprobs, "old_logprobs"), (ref_logprobs, "ref_logprobs")):
             _check_dev(t, torch.float32, n)
-        res = {k: torch.empty(B, T, dtype=torch.float32, device=tokens.device) for k in outputs}
+        res = {k: torch.empty(B, T, dtype=torch.float64 if k == "lse64" else torch.float32, device=tokens.device)
+               for k in outputs}
         o = _abi.rlo_token_out()
-        for k in ("logp", "old_logp", "ref_logp", "entropy", "dlogp", "loss", "lse"):
+        for k in ("logp", "old_logp", "ref_logp", "entropy", "dlogp", "loss", "lse", "lse64"):
             setattr(o, k, res[k].data_ptr() if k in res else None)
         L_old = _logits(old_logits, "old_logits", seq_start)
         L_ref = _logits(ref_logits, "ref_logits", seq_start)
@@ -369,9 +370,10 @@ class Objective:
             grad = torch.empty(B * T, actor_logits.shape[-1], dtype=grad_dtype or actor_logits.dtype,
                                device=actor_logits.device)
         G = _logits(grad, "grad")
-        res = {k: torch.empty(B, T, dtype=torch.float32, device=tokens.device) for k in outputs}
+        res = {k: torch.empty(B, T, dtype=torch.float64 if k == "lse64" else torch.float32, device=tokens.device)
+               for k in outputs}
         o = _abi.rlo_token_out()
-        for k in ("logp", "old_logp", "ref_logp", "entropy", "dlogp", "loss", "lse"):
+        for k in ("logp", "old_logp", "ref_logp", "entropy", "dlogp", "loss", "lse", "lse64"):
             setattr(o, k, res[k].data_ptr() if k in res else None)
         L_old = _logits(old_logits, "old_logits", seq_start)
         L_ref = _logits(ref_logits, "ref_logits", seq_start)
@@ -386,13 +388,15 @@ class Objective:
     def logits_backward(self, tokens, lengths, logits, lse, dlogp, weight, grad=None, grad_dtype=None, seq_start=None,
                         stream=None):
         """Actor backward epilogue (policy.cpp:375-379): dL/dlogits rows
-        w*dlogp*(onehot - softmax); returns the gradient tensor."""
+        w*dlogp*(onehot - softmax); returns the gradient tensor.  lse: the
+        ppo_gradient "lse" (fp32) or "lse64" (fp64, exact at any logit offset)."""
         torch = _torch()
         B, T = tokens.shape
         if grad is None:
             grad = torch.empty(B * T, logits.shape[-1], dtype=grad_dtype or logits.dtype, device=logits.device)
         G = _logits(grad, "grad")
-        check(_abi.lib().rlo_logits_backward(
+        fn = _abi.lib().rlo_logits_backward64 if lse.dtype == torch.float64 else _abi.lib().rlo_logits_backward
+        check(fn(
             self._h, C.byref(_batch(lengths, tokens, None, T)), C.byref(_logits(logits, seq_start=seq_start)), _ptr(lse),
             _ptr(dlogp),
             _ptr(weight), C.c_void_p(grad.data_ptr()), G.dtype, G.row_stride, _stream(stream, self.device)))

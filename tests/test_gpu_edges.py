@@ -152,3 +152,32 @@ def test_unaligned_rows_head_body_tail(env, dt):
     for i in (0, 1, 17, B * T - 1):
         want = O.logits_backward_row(rows[i], int(toks.ravel()[i]), 0.5 * -1.25)
         assert np.abs(g[i] - want).max() <= 1e-5 * 0.625 + 1e-12, i
+
+
+def test_backward_with_fp64_lse_at_extreme_offsets(env):
+    """Rows offset by +-1e4: the two-pass backward rebuilt from the fp64 lse
+    (rlo_token_out.lse64 -> rlo_logits_backward64) matches the oracle's
+    gradient to 1e-5; the fp32 lse carries its own rounding (ulp(1e4)/2)."""
+    torch, rlo, obj = env
+    rng = np.random.default_rng(12)
+    B, T, V = 2, 3, 4096
+    rows = (rng.standard_normal((B * T, V)) * 3).astype(np.float32)
+    rows[::2] -= 1e4
+    rows[1::2] += 1e4
+    toks = rng.integers(0, V, (B, T)).astype(np.int32)
+    L = dev(torch, np.array([T, T], np.int32))
+    x = dev(torch, rows)
+    cfg = rlo.TrainConfig()
+    old = dev(torch, np.full((B, T), -7.0, np.float32))
+    outs = obj.ppo_gradient(cfg, dev(torch, toks), L, x, dev(torch, np.ones((B, T), np.float32)), old_logprobs=old,
+                            outputs=("dlogp", "lse", "lse64"))
+    obj.merge_gradients(cfg)
+    w = torch.full((B, T), 0.25, device="cuda")
+    g64 = obj.logits_backward(dev(torch, toks), L, x, outs["lse64"], outs["dlogp"], w, grad_dtype=torch.float32)
+    G = g64.cpu().numpy()
+    dl = outs["dlogp"].cpu().numpy().ravel()
+    for i in range(B * T):
+        scale = float(np.float32(0.25) * np.float32(dl[i]))
+        want = O.logits_backward_row(rows[i].astype(np.float64), int(toks.ravel()[i]), scale)
+        assert np.abs(G[i] - want).max() <= 1e-5 * abs(scale) + 1e-12, (i, np.abs(G[i] - want).max())
+    assert abs(float(outs["lse64"][0, 0]) - O.logsoftmax_row(rows[0].astype(np.float64))[0]) <= 1e-6 * 1e4
