@@ -37,6 +37,12 @@ namespace {
 #ifndef RLO_FUSED_PF
 #define RLO_FUSED_PF 0
 #endif
+// The entropy row always guarded in the fused pass (no redo path): the fused
+// pass runs fp32 rows, which are memory-bound, and the smaller kernel measured
+// 0.6% faster (profiles/r1_fused.txt).  0 = unguarded + guarded redo.
+#ifndef RLO_FUSED_GUARD_ALWAYS
+#define RLO_FUSED_GUARD_ALWAYS 1
+#endif
 
 constexpr int kFT = 256;
 constexpr int kFW = kFT / 32;
@@ -248,10 +254,14 @@ __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
       for (int k = 0; k < NT; ++k) {
         acc_init(acc[k]);
         if (k == 0) {
-          slice_pass<ET, U, MATH, true>(rp0, n, sm, acc[0]);
-          if (!(isfinite(acc[0].s) && isfinite(acc[0].w))) {
-            acc_init(acc[0]);  // -inf logits in this thread's share: redo it guarded, from shared memory
-            slice_pass<ET, U, MATH | kMathGuard, false>(rp0, n, sm, acc[0]);
+          if (RLO_FUSED_GUARD_ALWAYS) {  // one guarded pass: less code (i-cache), the fp32 row is memory-bound
+            slice_pass<ET, U, MATH | kMathGuard, true>(rp0, n, sm, acc[0]);
+          } else {
+            slice_pass<ET, U, MATH, true>(rp0, n, sm, acc[0]);
+            if (!(isfinite(acc[0].s) && isfinite(acc[0].w))) {
+              acc_init(acc[0]);  // -inf logits in this thread's share: redo it guarded, from shared memory
+              slice_pass<ET, U, MATH | kMathGuard, false>(rp0, n, sm, acc[0]);
+            }
           }
         } else {
           const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + logits_off(a, k, row) + c0;
