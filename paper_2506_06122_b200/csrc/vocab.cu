@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
       acc_init(acc[k]);
       const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + logits_off(a, k, row);
       if (k == 0 && ENT0) {
-        if (RLO_ENT_GUARD_ALWAYS) {
+        if (RLO_ENT_GUARD_ALWAYS || sizeof(ET) == 4) {  // fp32 rows are memory-bound: one guarded body
           stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, acc[k]);
         } else {
           stream_accumulate<kThreads, ET, U, PF, true, MATH>(rp, a.V, acc[k]);
