@@ -437,8 +437,9 @@ cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
   if ((int64_t)a.B * a.T == 0) return cudaSuccess;
   const int math = env_int("RLO_VOCAB_MATH", sizeof(ET) == 2 ? 6 : 1);
   if constexpr (sizeof(ET) == 4) {
-    return math == 0 ? launch_impl<ET, NT, LOSS, ENT0, 0>(a, num_sms, s)
-                     : launch_impl<ET, NT, LOSS, ENT0, 1>(a, num_sms, s);
+    return math == 0   ? launch_impl<ET, NT, LOSS, ENT0, 0>(a, num_sms, s)
+           : math == 2 ? launch_impl<ET, NT, LOSS, ENT0, 1 | kMathLazy>(a, num_sms, s)
+                       : launch_impl<ET, NT, LOSS, ENT0, 1>(a, num_sms, s);
   } else {
     switch (math) {
       case 1: return launch_impl<ET, NT, LOSS, ENT0, 1>(a, num_sms, s);
@@ -446,6 +447,8 @@ cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
       case 4: return launch_impl<ET, NT, LOSS, ENT0, 4>(a, num_sms, s);
       case 5: return launch_impl<ET, NT, LOSS, ENT0, 5>(a, num_sms, s);
       case 6: return launch_impl<ET, NT, LOSS, ENT0, 6>(a, num_sms, s);
+      case 7: return launch_impl<ET, NT, LOSS, ENT0, 6 | kMathLazy>(a, num_sms, s);
+      case 8: return launch_impl<ET, NT, LOSS, ENT0, 1 | kMathLazy>(a, num_sms, s);
       default: return launch_impl<ET, NT, LOSS, ENT0, 2>(a, num_sms, s);
     }
   }

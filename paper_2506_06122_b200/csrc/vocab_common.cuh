@@ -105,6 +105,17 @@ constexpr int kMathGuard = 0x100;
 // kMathNoMax: the caller already rescaled the state to a shared running max
 // (lockstep streams of several tensors, vocab.cu); skip the per-chunk max.
 constexpr int kMathNoMax = 0x200;
+// kMathLazy: once a thread's state holds a real running max, a chunk is first
+// summed against that max without taking the chunk max; only if the chunk sum
+// reaches kLazyCap (an element more than ~27 log2 units above the running
+// max, or a non-finite value) is the chunk redone the exact way (chunk max,
+// rescale, sum).  The offset of an online log-sum-exp need not be the maximum
+// -- any offset that keeps the terms finite gives the same lse and entropy
+// (H = log2 s - w/s holds for every offset) -- so this drops the per-element
+// max (one HMNMX2 / FMNMX per pair) from almost every chunk.
+constexpr int kMathLazy = 0x400;
+constexpr float kLazyCap = 4294967296.0f;  // 2^32
+constexpr float kLazyMin = -1.0e29f;      // mL above this holds a real max (init is kNegInit * kL2E)
 
 // GUARD (entropy row): clamp t so that -inf logits (masked vocabulary
 // entries) give e*t = 2^-126 * -126 (negligible) instead of 0 * -inf = NaN.
@@ -134,6 +145,27 @@ __device__ __forceinline__ float hsum2(f2 a, f2 b) {
 template <typename ET>
 struct Vec;
 
+// One chunk (U 16-byte vectors) into the online state: chunk max + rescale,
+// then the sums (or, under kMathLazy, the sums against the current max first).
+template <typename VT, int U, bool ENT, int MATHG>
+__device__ __forceinline__ void accumulate_chunk(const typename VT::V (&v)[U], Acc& a) {
+  float cs, cw = 0.f;
+  if (MATHG & kMathLazy) {
+    if (a.mL > kLazyMin) {
+      VT::template sums<U, ENT, MATHG>(v, a.mL, cs, cw);
+      if (cs < kLazyCap) {  // false for inf / NaN: those chunks take the exact path below
+        a.s += cs;
+        if (ENT) a.w += cw;
+        return;
+      }
+    }
+  }
+  if (!(MATHG & kMathNoMax)) acc_rescale<ENT>(a, VT::template chunk_max<U>(v));
+  VT::template sums<U, ENT, MATHG>(v, a.mL, cs, cw);
+  a.s += cs;
+  if (ENT) a.w += cw;
+}
+
 template <>
 struct Vec<float> {
   using V = float4;
@@ -150,33 +182,37 @@ struct Vec<float> {
     for (int u = 1; u < U; ++u) m = fmaxf(m, fmaxf(fmaxf(v[u].x, v[u].y), fmaxf(v[u].z, v[u].w)));
     return m;
   }
+  // The chunk's sums relative to the offset mL (no max, no state update).
   template <int U, bool ENT, int MATHG>
-  __device__ static void accumulate(const V (&v)[U], Acc& a) {
+  __device__ static void sums(const V (&v)[U], float mL, float& cs, float& cw) {
     constexpr int MATH = MATHG & kMathMask;
     constexpr bool G = (MATHG & kMathGuard) != 0;
-    if (!(MATHG & kMathNoMax)) acc_rescale<ENT>(a, chunk_max<U>(v));
     if (MATH == 0) {
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, w0 = 0.f, w1 = 0.f, w2 = 0.f, w3 = 0.f;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        acc_elem<ENT>(v[u].x, a.mL, s0, w0);
-        acc_elem<ENT>(v[u].y, a.mL, s1, w1);
-        acc_elem<ENT>(v[u].z, a.mL, s2, w2);
-        acc_elem<ENT>(v[u].w, a.mL, s3, w3);
+        acc_elem<ENT>(v[u].x, mL, s0, w0);
+        acc_elem<ENT>(v[u].y, mL, s1, w1);
+        acc_elem<ENT>(v[u].z, mL, s2, w2);
+        acc_elem<ENT>(v[u].w, mL, s3, w3);
       }
-      a.s += (s0 + s1) + (s2 + s3);
-      if (ENT) a.w += (w0 + w1) + (w2 + w3);
+      cs = (s0 + s1) + (s2 + s3);
+      if (ENT) cw = (w0 + w1) + (w2 + w3);
     } else {
-      const f2 L2 = pk2(kL2E, kL2E), nmL = pk2(-a.mL, -a.mL);
+      const f2 L2 = pk2(kL2E, kL2E), nmL = pk2(-mL, -mL);
       f2 s0 = 0, s1 = 0, w0 = 0, w1 = 0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         pair2<ENT, G>(v[u].x, v[u].y, L2, nmL, s0, w0, 0);
         pair2<ENT, G>(v[u].z, v[u].w, L2, nmL, s1, w1, (!ENT && (u & 1)) ? poly_deg(MATH) : 0);
       }
-      a.s += hsum2(s0, s1);
-      if (ENT) a.w += hsum2(w0, w1);
+      cs = hsum2(s0, s1);
+      if (ENT) cw = hsum2(w0, w1);
     }
+  }
+  template <int U, bool ENT, int MATHG>
+  __device__ static void accumulate(const V (&v)[U], Acc& a) {
+    accumulate_chunk<Vec<float>, U, ENT, MATHG>(v, a);
   }
   __device__ static float scalar(const float* p) { return __ldg(p); }
 };
@@ -201,23 +237,22 @@ struct Vec<__nv_bfloat16> {
     acc_elem<ENT>(bf16hi(x), mL, s1, w1);
   }
   template <int U, bool ENT, int MATHG>
-  __device__ static void accumulate(const V (&v)[U], Acc& a) {
+  __device__ static void sums(const V (&v)[U], float mL, float& cs, float& cw) {
     constexpr int MATH = MATHG & kMathMask;
     constexpr bool G = (MATHG & kMathGuard) != 0;
-    if (!(MATHG & kMathNoMax)) acc_rescale<ENT>(a, chunk_max<U>(v));
     if (MATH == 0) {
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, w0 = 0.f, w1 = 0.f, w2 = 0.f, w3 = 0.f;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        word<ENT>(v[u].x, a.mL, s0, s1, w0, w1);
-        word<ENT>(v[u].y, a.mL, s2, s3, w2, w3);
-        word<ENT>(v[u].z, a.mL, s0, s1, w0, w1);
-        word<ENT>(v[u].w, a.mL, s2, s3, w2, w3);
+        word<ENT>(v[u].x, mL, s0, s1, w0, w1);
+        word<ENT>(v[u].y, mL, s2, s3, w2, w3);
+        word<ENT>(v[u].z, mL, s0, s1, w0, w1);
+        word<ENT>(v[u].w, mL, s2, s3, w2, w3);
       }
-      a.s += (s0 + s1) + (s2 + s3);
-      if (ENT) a.w += (w0 + w1) + (w2 + w3);
+      cs = (s0 + s1) + (s2 + s3);
+      if (ENT) cw = (w0 + w1) + (w2 + w3);
     } else {
-      const f2 L2 = pk2(kL2E, kL2E), nmL = pk2(-a.mL, -a.mL);
+      const f2 L2 = pk2(kL2E, kL2E), nmL = pk2(-mL, -mL);
       f2 s0 = 0, s1 = 0, w0 = 0, w1 = 0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -226,9 +261,13 @@ struct Vec<__nv_bfloat16> {
         pair2<ENT, G>(bf16lo(v[u].z), bf16hi(v[u].z), L2, nmL, s0, w0, 0);
         pair2<ENT, G>(bf16lo(v[u].w), bf16hi(v[u].w), L2, nmL, s1, w1, (ENT || !poly_half(MATH)) ? 0 : poly_deg(MATH));
       }
-      a.s += hsum2(s0, s1);
-      if (ENT) a.w += hsum2(w0, w1);
+      cs = hsum2(s0, s1);
+      if (ENT) cw = hsum2(w0, w1);
     }
+  }
+  template <int U, bool ENT, int MATHG>
+  __device__ static void accumulate(const V (&v)[U], Acc& a) {
+    accumulate_chunk<Vec<__nv_bfloat16>, U, ENT, MATHG>(v, a);
   }
   __device__ static float scalar(const __nv_bfloat16* p) {
     return __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(p)));

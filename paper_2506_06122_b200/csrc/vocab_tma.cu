@@ -222,14 +222,17 @@ cudaError_t launch_tma(const VocabArgs& a, int num_sms, cudaStream_t s) {
   template cudaError_t launch_tma<ET, NT, LOSS, ENT0, M>(const VocabArgs&, int, cudaStream_t);
 #define RLO_INST_F(NT, LOSS, ENT0)         \
   RLO_INST1(float, NT, LOSS, ENT0, 0)     \
-  RLO_INST1(float, NT, LOSS, ENT0, 1)
+  RLO_INST1(float, NT, LOSS, ENT0, 1)     \
+  RLO_INST1(float, NT, LOSS, ENT0, 1 | kMathLazy)
 #define RLO_INST_B(NT, LOSS, ENT0)                 \
   RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 1)     \
   RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 2)     \
   RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 3)     \
   RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 4)     \
   RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 5)     \
-  RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 6)
+  RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 6)     \
+  RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 6 | kMathLazy) \
+  RLO_INST1(__nv_bfloat16, NT, LOSS, ENT0, 1 | kMathLazy)
 RLO_INST_F(1, false, false)
 RLO_INST_F(1, false, true)
 RLO_INST_F(1, true, true)
