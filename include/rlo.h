@@ -397,9 +397,14 @@ rlo_status rlo_value_loss(rlo_handle* h, const rlo_batch* batch, const float* va
  * reference's keyed uniform u = keyed_double({seed, version, sample_key[i],
  * position[i]}) (rng.hpp:82-85), returning the token and its UNtempered
  * log-prob (policy.cpp:168), i.e. response_logprobs, so the PPO ratio needs
- * no separate old-policy logits pass.  Tempered weights in fp64 like the
- * reference (the token is the reference's unless u*total falls within fp64
- * rounding of a CDF boundary); the untempered log-sum-exp in fp32.
+ * no separate old-policy logits pass.  The token is the fp64 CDF walk's (the
+ * reference's unless u*total falls within fp64 rounding of a CDF boundary):
+ * an fp32 screen certifies most draws (u*total more than an error bound away
+ * from the picked token's CDF boundaries), the rest are redone with fp64
+ * weights; the untempered log-sum-exp in fp32.  Two kernel launches, no host
+ * synchronisation; out_tokens is written twice (uncertified rows hold -1
+ * between the launches).  RLO_DECODE_MARGIN overrides the certificate margin
+ * (<= 0: fp64 only).
  * sample_keys / positions [n_rows] device uint64; out_tokens int32 [n_rows];
  * out_logp float [n_rows].  ConfigError for temperature <= 0 (policy.cpp:146). */
 rlo_status rlo_decode_sample(rlo_handle* h, const rlo_logits* logits, int32_t n_rows, double temperature,

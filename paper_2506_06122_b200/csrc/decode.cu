@@ -11,9 +11,34 @@
 // rounding of a CDF boundary), through a table-driven exp (exp_neg); the
 // UNtempered log-sum-exp only feeds the returned log-prob and runs in fp32 in
 // log2 units like the vocab pass (relative error ~1e-7).
-// Traffic per row ~ (1 + 1/8) x V x s; bound by fp64 throughput (~13 fp64
-// operations per element).
+// Traffic per row ~ (1 + 1/8) x V x s.
+//
+// Two paths per row.  The screened fp32 path (default) computes the tempered
+// weights 2^(z*cT - mT) with MUFU.EX2 in fp32 (vector sums of 4-8 accumulated
+// in fp64), walks the CDF the same way, and accepts its pick only with a
+// certificate: the threshold X = u * total lies more than margin * total
+// inside the picked token's CDF interval, margin = 2.5 x eps(V), where eps(V)
+// bounds the error of every fp32-derived CDF value and of X relative to the
+// total (screen_margin below):
+//   argument rounding, |dt| <= |t| 2^-24 per term, and the fp32 constant
+//   cT = log2(e)/T, |dt| <= |t| 2^-24: sum_v w_v |t_v| ln2 2^-24 each, and
+//   sum_v w_v |t_v| <= total * log2(V) (sum p (-log2 p) <= log2 V, the max
+//   weight being 1);
+//   ex2.approx.ftz.f32 <= 1.44e-7 relative (exhaustive over t in [-126, 1] on
+//   B200, tools/probes/ex2_probe.cu; 1.5e-7 used); the fp32 vector tree
+//   <= 3 * 2^-24; fp64 accumulation and the fp64 rescales negligible.
+// Under the certificate the exact CDF walk picks the same token, so the draw
+// is the fp64 path's.  A row without one (a CDF boundary within the margin,
+// most likely on flat rows: 5-23% of synthetic Qwen-vocabulary draws at
+// T = 0.6-1.0, profiles/r1_next_rows.txt; or non-finite sums) is redone by the
+// fp64 path — the weights exp((z - m)/T) in fp64 through a table-driven exp
+// (exp_neg), bound by fp64 throughput (~13 fp64 operations per element) — in
+// a second launch that skips the certified rows.  RLO_DECODE_MARGIN overrides
+// the margin (<= 0: fp64 path only; >= 1: every row redone, for tests).
 #include <cuda_bf16.h>
+
+#include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -119,6 +144,250 @@ __device__ __forceinline__ void load_e(const ET* z, int v, int lim, bool vec_ok,
   }
 }
 
+// The certificate margin (relative to the total) for a vocabulary of V tokens.
+inline double screen_margin(int V) {
+  const double u = 0x1p-24;
+  const double eps = 2.0 * std::log2((double)(V > 2 ? V : 2)) * u * 0.6931471805599453 + 1.5e-7 + 3.0 * u;
+  return 2.5 * eps;
+}
+#ifndef RLO_SCREEN_U
+#define RLO_SCREEN_U 4
+#endif
+#ifndef RLO_SCREEN_MINB
+#define RLO_SCREEN_MINB 4
+#endif
+constexpr int kScreenU = RLO_SCREEN_U;  // 16-byte loads in flight per lane (screened path)
+constexpr int kStepMax = 1024;     // step sums of one warp range kept in shared memory
+
+// Raw 16-byte vectors of E logits (token order) and their fp32 values.
+template <typename ET>
+struct RawVec;
+template <>
+struct RawVec<float> {
+  static constexpr int E = 4;
+  static constexpr uint32_t kNegInf = 0xFF800000u;
+  __device__ static float at(const uint4& r, int e) {
+    return __uint_as_float(e == 0 ? r.x : e == 1 ? r.y : e == 2 ? r.z : r.w);
+  }
+  __device__ static uint32_t raw1(const float* z, int v) { return __float_as_uint(__ldg(z + v)); }
+  __device__ static uint4 fill(const float* z, int v, int lim) {
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) w[e] = v + e < lim ? raw1(z, v + e) : kNegInf;
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+template <>
+struct RawVec<__nv_bfloat16> {
+  static constexpr int E = 8;
+  __device__ static float at(const uint4& r, int e) {
+    const uint32_t w = (e >> 1) == 0 ? r.x : (e >> 1) == 1 ? r.y : (e >> 1) == 2 ? r.z : r.w;
+    return (e & 1) ? bf16hi(w) : bf16lo(w);
+  }
+  __device__ static uint32_t raw1(const __nv_bfloat16* z, int v) {
+    return (uint32_t)__ldg(reinterpret_cast<const unsigned short*>(z) + v);
+  }
+  __device__ static uint4 fill(const __nv_bfloat16* z, int v, int lim) {
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t lo = v + 2 * k < lim ? raw1(z, v + 2 * k) : 0xFF80u;
+      const uint32_t hi = v + 2 * k + 1 < lim ? raw1(z, v + 2 * k + 1) : 0xFF80u;
+      w[k] = lo | (hi << 16);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+// Tokens [v, v+E) of the row, -inf past lim: one 16-byte load when the
+// vector is whole and aligned, else per element.
+template <typename ET>
+__device__ __forceinline__ uint4 load_raw(const ET* z, int v, int lim, bool vec_ok) {
+  if (vec_ok && v + RawVec<ET>::E <= lim) return ld_stream(reinterpret_cast<const uint4*>(z + v));
+  return v < lim ? RawVec<ET>::fill(z, v, lim) : RawVec<ET>::fill(z, lim, lim);
+}
+
+// fp32 sum of the E weights 2^(x*c - mo) of one vector (3-level tree), in fp64.
+template <typename ET>
+__device__ __forceinline__ double vec_wsum(const uint4& r, float c, float mo) {
+  constexpr int E = RawVec<ET>::E;
+  float w[8];
+#pragma unroll
+  for (int e = 0; e < E; ++e) w[e] = ex2(fmaf(RawVec<ET>::at(r, e), c, -mo));  // -inf -> 0
+#pragma unroll
+  for (int h = E / 2; h > 0; h >>= 1) {
+#pragma unroll
+    for (int e = 0; e < h; ++e) w[e] += w[e + h];
+  }
+  return (double)w[0];
+}
+
+// The screened fp32 path for one row (every thread of the CTA calls it; the
+// result is uniform).  Weights 2^(z*cT - mT): cT = log2(e)/T as fp32, mT the
+// rounded max times cT (a common factor, exact across rescales, which the
+// CDF walk does not see).
+//   pass 1: warp j owns tokens [j*W, (j+1)*W); per lane kScreenU 16-byte
+//           loads in flight; running max, tempered and untempered sums
+//           (fp32 vector sums accumulated in fp64);
+//   thread 0: totals, lse, X = u * total, the crossing warp range;
+//   pass 2a: the 8 warps sum the crossing range's steps of 32*E tokens
+//           (kScreenU steps in flight per warp) into shared memory;
+//   warp 0: scans the step sums for the crossing step, walks it (warp prefix
+//           of the lane sums, then the hit lane's tokens in order) and checks
+//           the certificate X - CDF(c-1) > margin * total, CDF(c) - X > margin * total.
+// Returns true with s_pick / s_lse set when the certificate holds; false
+// sends the row to the fp64 path.
+template <typename ET>
+__device__ __forceinline__ bool screened_row(const ET* __restrict__ z, int V, int W, bool vec_ok, bool unit_t, float cT,
+                                             double margin, double u, double* s_t, double* s_u2, float* s_mt,
+                                             float* s_ml, double* s_step, double& s_thresh, double& s_total,
+                                             double& s_lse, int& s_warp, int& s_pick, int& s_ok) {
+  constexpr int E = RawVec<ET>::E, S = 32 * E, U = kScreenU;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int v0 = warp * W, v1 = min(V, v0 + W);
+  float m = -INFINITY, mL = kNegInit * kL2E, mT = kNegInit * kL2E;
+  double st = 0.0, su = 0.0;
+  for (int b = v0 + lane * E; b < v1; b += U * S) {
+    uint4 r[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) r[k] = load_raw<ET>(z, b + k * S, v1, vec_ok);
+    float cm = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+#pragma unroll
+      for (int e = 0; e < E; ++e) cm = fmaxf(cm, RawVec<ET>::at(r[k], e));
+    if (cm > m) {
+      const float nL = __fmul_rn(cm, kL2E), nT = unit_t ? nL : __fmul_rn(cm, cT);
+      su *= exp2((double)mL - (double)nL);
+      st *= exp2((double)mT - (double)nT);
+      m = cm, mL = nL, mT = nT;
+    }
+    if (m == -INFINITY) continue;
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const double qs = vec_wsum<ET>(r[k], kL2E, mL);
+      su += qs;
+      st += unit_t ? qs : vec_wsum<ET>(r[k], cT, mT);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ml2 = __shfl_xor_sync(0xffffffffu, mL, o), mt2 = __shfl_xor_sync(0xffffffffu, mT, o);
+    const double su2 = __shfl_xor_sync(0xffffffffu, su, o), st2 = __shfl_xor_sync(0xffffffffu, st, o);
+    const float ML = fmaxf(mL, ml2), MT = fmaxf(mT, mt2);
+    su = su * exp2((double)mL - ML) + su2 * exp2((double)ml2 - ML);
+    st = st * exp2((double)mT - MT) + st2 * exp2((double)mt2 - MT);
+    mL = ML, mT = MT;
+  }
+  if (lane == 0) s_t[warp] = st, s_u2[warp] = su, s_mt[warp] = mT, s_ml[warp] = mL;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float MT = s_mt[0], ML = s_ml[0];
+    for (int j = 1; j < kDecWarps; ++j) MT = fmaxf(MT, s_mt[j]), ML = fmaxf(ML, s_ml[j]);
+    double T = 0.0, Uu = 0.0;
+    for (int j = 0; j < kDecWarps; ++j) {
+      s_t[j] *= exp2((double)s_mt[j] - MT);
+      T += s_t[j];
+      Uu += s_u2[j] * exp2((double)s_ml[j] - ML);
+    }
+    const double X = u * T, mg = margin * T;
+    int jw = -1;
+    double base = 0.0;
+    // a threshold within the margin of the total (the reference's no-crossing
+    // fallback to the last token is in play) or non-finite sums: fp64 path
+    if (isfinite(T) && T > 0.0 && isfinite(Uu) && Uu > 0.0 && X < T - mg && W / S <= kStepMax) {
+      for (int j = 0; j < kDecWarps; ++j) {
+        if (X < base + s_t[j]) {
+          jw = j;
+          break;
+        }
+        base += s_t[j];
+      }
+    }
+    s_warp = jw;
+    s_u2[0] = base;  // CDF before the crossing warp range
+    s_thresh = X;
+    s_total = T;
+    s_mt[0] = MT;
+    s_lse = ((double)ML + log2(Uu)) / (double)kL2E;
+    s_ok = 0;
+  }
+  __syncthreads();
+  const int jw = s_warp;
+  if (jw < 0) return false;
+  const float MT = s_mt[0];
+  const int a0 = jw * W, a1 = min(V, a0 + W);
+  const int nsteps = (a1 - a0 + S - 1) / S;
+  // pass 2a: step sums of the crossing range, U steps in flight per warp
+  for (int s0 = warp; s0 < nsteps; s0 += U * kDecWarps) {
+    uint4 r[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) r[k] = load_raw<ET>(z, a0 + (s0 + k * kDecWarps) * S + lane * E, a1, vec_ok);
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const double ls = warp_sum(vec_wsum<ET>(r[k], cT, MT));
+      const int sk = s0 + k * kDecWarps;
+      if (lane == 0 && sk < nsteps) s_step[sk] = ls;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const double X = s_thresh, mg = margin * s_total;
+    double base = s_u2[0];
+    int ks = -1;
+    for (int c = 0; c < nsteps && ks < 0; c += 32) {  // first step whose inclusive CDF passes X
+      const double v = c + lane < nsteps ? s_step[c + lane] : 0.0;
+      double incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double q = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += q;
+      }
+      const unsigned hit = __ballot_sync(0xffffffffu, c + lane < nsteps && X < base + incl);
+      if (hit) {
+        const int hl = __ffs(hit) - 1;
+        ks = c + hl;
+        base += __shfl_sync(0xffffffffu, incl - v, hl);
+      } else {
+        base += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+    if (ks >= 0) {  // walk step ks (else the sums disagree at a range boundary: fp64 path)
+      const int b = a0 + ks * S + lane * E;
+      const uint4 r = load_raw<ET>(z, b, a1, vec_ok);
+      float w[8];
+      double ls = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        w[e] = ex2(fmaf(RawVec<ET>::at(r, e), cT, -MT));
+        ls += (double)w[e];
+      }
+      double incl = ls;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double q = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += q;
+      }
+      const unsigned hit = __ballot_sync(0xffffffffu, b < a1 && X < base + incl);
+      if (hit && lane == __ffs(hit) - 1) {
+        double a = base + incl - ls;  // CDF before this lane's first token
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const double prev = a;
+          a += (double)w[e];
+          if (b + e < a1 && X < a) {
+            // the certificate: X more than margin * total inside (CDF(c-1), CDF(c)]
+            s_pick = b + e;
+            s_ok = (X - prev > mg && a - X > mg) ? 1 : 0;
+            break;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
 // One CTA per row, 8 warps; warp j owns the contiguous token range
 // [j*W, (j+1)*W), W a multiple of 32*E; lane l takes the E consecutive tokens
 // at base + l*E of each 32*E step (16-byte loads, token order preserved).
@@ -136,14 +405,15 @@ template <typename ET>
 __global__ void __launch_bounds__(kDecWarps * 32)
     decode_kernel(const ET* __restrict__ logits, int64_t stride, int V, int n, double temp, uint64_t seed,
                   uint64_t version, const uint64_t* __restrict__ keys, const uint64_t* __restrict__ positions,
-                  int32_t* __restrict__ out_tok, float* __restrict__ out_lp) {
+                  int32_t* __restrict__ out_tok, float* __restrict__ out_lp, bool redo_only) {
   constexpr int E = DVec<ET>::E;
   __shared__ double tab[kExpTab];
   __shared__ double s_t[kDecWarps];
   __shared__ float s_m[kDecWarps], s_ml[kDecWarps], s_su[kDecWarps];
-  __shared__ double s_base, s_thresh, s_lse;
+  __shared__ double s_base, s_thresh, s_lse, s_total;
   __shared__ float s_M;
   __shared__ int s_warp, s_pick;
+
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int j = threadIdx.x; j < kExpTab; j += blockDim.x) tab[j] = exp2((double)j / kExpTab);
   __syncthreads();
@@ -155,6 +425,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   for (int row = blockIdx.x; row < n; row += gridDim.x) {
     const ET* z = logits + (int64_t)row * stride;
     const int v0 = warp * W, v1 = min(V, v0 + W);
+    if (redo_only && out_tok[row] >= 0) continue;  // the screened kernel certified this row
     // pass 1
     float m = -INFINITY, mL = kNegInit * kL2E, su = 0.f, lo = -INFINITY;
     double st = 0.0;
@@ -342,6 +613,36 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   }
 }
 
+// The screened pass over every row: the certified rows get their token and
+// log-prob; the others are marked out_tok = -1 for the fp64 kernel's redo.
+template <typename ET>
+__global__ void __launch_bounds__(kDecWarps * 32, RLO_SCREEN_MINB)
+    decode_screen_kernel(const ET* __restrict__ logits, int64_t stride, int V, int n, double temp, uint64_t seed,
+                         uint64_t version, const uint64_t* __restrict__ keys, const uint64_t* __restrict__ positions,
+                         int32_t* __restrict__ out_tok, float* __restrict__ out_lp, double margin) {
+  constexpr int E = RawVec<ET>::E;
+  __shared__ double s_t[kDecWarps], s_u2[kDecWarps];
+  __shared__ double s_step[kStepMax];
+  __shared__ float s_mt[kDecWarps], s_ml[kDecWarps];
+  __shared__ double s_thresh, s_total, s_lse;
+  __shared__ int s_warp, s_pick, s_ok;
+  const bool unit_t = temp == 1.0;
+  const float cT = unit_t ? kL2E : (float)((double)kL2E / temp);  // tempered log2 scale
+  const int W = ((V + kDecWarps - 1) / kDecWarps + 32 * E - 1) / (32 * E) * (32 * E);
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(logits) & 15u) == 0) && (((stride * (int64_t)sizeof(ET)) & 15) == 0);
+  for (int row = blockIdx.x; row < n; row += gridDim.x) {
+    const ET* z = logits + (int64_t)row * stride;
+    const bool ok = screened_row<ET>(z, V, W, vec_ok, unit_t, cT, margin,
+                                     keyed_double4(seed, version, keys[row], positions[row]), s_t, s_u2, s_mt, s_ml,
+                                     s_step, s_thresh, s_total, s_lse, s_warp, s_pick, s_ok);
+    if (threadIdx.x == 0) {
+      out_tok[row] = ok ? s_pick : -1;
+      if (ok) out_lp[row] = (float)((double)logit(z, s_pick) - s_lse);  // untempered logp (policy.cpp:168)
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_decode(const void* logits, int32_t dtype, int64_t stride, int32_t V, int32_t n, double temperature,
@@ -349,14 +650,31 @@ cudaError_t launch_decode(const void* logits, int32_t dtype, int64_t stride, int
                           int32_t* out_tok, float* out_lp, int num_sms, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const int grid = n < num_sms * 8 ? n : num_sms * 8;
-  if (dtype == RLO_DTYPE_BF16)
+  const char* me = std::getenv("RLO_DECODE_MARGIN");
+  const double margin = (me && *me) ? std::atof(me) : screen_margin(V);
+  const bool bf = dtype == RLO_DTYPE_BF16;
+  if (margin > 0.0) {
+    if (bf)
+      decode_screen_kernel<__nv_bfloat16><<<grid, kDecWarps * 32, 0, s>>>(
+          reinterpret_cast<const __nv_bfloat16*>(logits), stride, V, n, temperature, seed, version, keys, positions,
+          out_tok, out_lp, margin);
+    else
+      decode_screen_kernel<float><<<grid, kDecWarps * 32, 0, s>>>(reinterpret_cast<const float*>(logits), stride, V,
+                                                                  n, temperature, seed, version, keys, positions,
+                                                                  out_tok, out_lp, margin);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  const bool redo = margin > 0.0;  // the fp64 kernel redoes only the rows the screen left (out_tok = -1)
+  const char* nr = std::getenv("RLO_DECODE_NOREDO");  // diagnostics: leave the screen's -1 marks (fail rate)
+  if (redo && nr && *nr == '1') return cudaGetLastError();
+  if (bf)
     decode_kernel<__nv_bfloat16><<<grid, kDecWarps * 32, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(logits), stride,
                                                                   V, n, temperature, seed, version, keys,
-                                                                  positions, out_tok, out_lp);
+                                                                  positions, out_tok, out_lp, redo);
   else
     decode_kernel<float><<<grid, kDecWarps * 32, 0, s>>>(reinterpret_cast<const float*>(logits), stride, V, n,
                                                          temperature, seed, version, keys, positions, out_tok,
-                                                         out_lp);
+                                                         out_lp, redo);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

@@ -192,3 +192,65 @@ def test_decode_sample_large_vocab_vs_oracle(env, dt, V, pad):
             want, want_lp = O.decode_next(ref_rows[i], temp, 99, 5, int(keys[i]), int(pos[i]))
             assert tok[i] == want, (temp, i)
             assert abs(lp[i] - want_lp) <= 1e-5 * max(1.0, abs(want_lp)), (temp, i, lp[i], want_lp)
+
+
+def _keyed_double_np(seed, version, keys, pos):
+    """rng::keyed_double({seed, version, key, position}) (rng.hpp:15-31, 82-85) for arrays of keys (uint64 wrap)."""
+    M = np.uint64
+    with np.errstate(over="ignore"):
+        def mix(state):
+            state = state + M(0x9E3779B97F4A7C15)
+            z = state
+            z = (z ^ (z >> M(30))) * M(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> M(27))) * M(0x94D049BB133111EB)
+            return state, z ^ (z >> M(31))
+        n = len(keys)
+        state = np.full(n, 0x2545F4914F6CDD1D, dtype=M)
+        state, h = mix(state)
+        for k in (np.full(n, seed, M), np.full(n, version, M), keys.astype(M), pos.astype(M)):
+            state = state ^ k
+            state, hk = mix(state)
+            h = h ^ hk
+        return (h >> M(11)).astype(np.float64) * 2.0 ** -53
+
+
+@pytest.mark.parametrize("dt,temp", [("f32", 1.0), ("bf16", 1.0), ("f32", 0.7), ("bf16", 1.3)])
+def test_decode_sample_cdf_boundary_draws(env, dt, temp, monkeypatch):
+    """Draws whose threshold u lies within 1e-9..1e-5 of a CDF boundary (keys
+    searched for it): the screened fp32 path must hand the rows inside its
+    certificate margin (3.3e-6 of the total at V = 4096) to the fp64 path and
+    certify the others, and the tokens equal the fp64 oracle's either way.  The same launch with the screen off
+    (RLO_DECODE_MARGIN=0) and with every row redone (=1) gives the same tokens."""
+    torch, rlo, obj = env
+    rng = np.random.default_rng(2024)
+    V, seed, ver = 4096, 11, 3
+    tdt = torch.float32 if dt == "f32" else torch.bfloat16
+    row = torch.from_numpy((rng.standard_normal(V) * 2).astype(np.float32)).to(tdt)
+    z = row.float().numpy().astype(np.float64)
+    p = np.exp((z - z.max()) / temp)
+    cdf = np.cumsum(p / p.sum())
+    cand = np.arange(1 << 20, dtype=np.uint64)
+    pos = np.full(cand.size, 5, np.uint64)
+    u = _keyed_double_np(seed, ver, cand, pos)
+    i = np.clip(np.searchsorted(cdf, u), 1, V - 1)
+    d = np.minimum(np.abs(cdf[i] - u), np.abs(cdf[i - 1] - u))
+    pick = []
+    for lo, hi in ((0, 1e-9), (1e-9, 1e-7), (1e-7, 1e-6), (1e-6, 1e-5), (1e-5, 3e-5)):
+        sel = np.nonzero((d >= lo) & (d < hi))[0][:8]
+        pick.extend(sel.tolist())
+    assert len(pick) >= 24
+    keys = cand[pick].astype(np.int64)
+    n = len(pick)
+    x = row.cuda().unsqueeze(0).expand(n, V).contiguous()
+    kd, pd = dev(torch, keys), dev(torch, np.full(n, 5, np.int64))
+    toks = {}
+    for mg in ("", "0", "1"):
+        monkeypatch.setenv("RLO_DECODE_MARGIN", mg)
+        t, lp = obj.decode_sample(x, temp, seed, ver, kd, pd)
+        toks[mg] = t.cpu().numpy()
+        lp = lp.cpu().numpy()
+        for j in range(n):
+            want, want_lp = O.decode_next(z, temp, seed, ver, int(keys[j]), 5)
+            assert toks[mg][j] == want, (mg, j, d[pick[j]])
+            assert abs(lp[j] - want_lp) <= 1e-5 * max(1.0, abs(want_lp))
+    monkeypatch.delenv("RLO_DECODE_MARGIN")

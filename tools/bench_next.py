@@ -48,12 +48,17 @@ def bench_decode(obj):
         rlo.synth_logits(x, seed=1, model=0)
         keys = torch.arange(rows, dtype=torch.int64, device="cuda") * 7919
         pos = torch.full((rows,), 17, dtype=torch.int64, device="cuda")
-        ms = timed(lambda: obj.decode_sample(x, 0.8, 42, 3, keys, pos))
         byts = rows * V * x.element_size()
-        print(json.dumps({"row": "decode", "rows": rows, "V": V, "stride": stride, "dtype": str(dt).split(".")[-1],
-                          "ms": ms,
-                          "rows_per_s": rows / ms * 1e3, "gbs_one_pass": byts / ms / 1e6,
-                          "note": "fp64 tempered CDF walk; bytes = one pass over each row"}), flush=True)
+        for temp in (0.8, 1.0):
+            for margin in ("", "0"):  # screened fp32 path (default) / fp64 path only
+                os.environ["RLO_DECODE_MARGIN"] = margin
+                ms = timed(lambda: obj.decode_sample(x, temp, 42, 3, keys, pos))
+                print(json.dumps({"row": "decode", "rows": rows, "V": V, "stride": stride,
+                                  "dtype": str(dt).split(".")[-1], "temperature": temp,
+                                  "path": "fp64" if margin == "0" else "screened", "ms": ms,
+                                  "rows_per_s": rows / ms * 1e3, "gbs_one_pass": byts / ms / 1e6,
+                                  "note": "bytes = one pass over each row"}), flush=True)
+        os.environ.pop("RLO_DECODE_MARGIN", None)
         del x
 
 
