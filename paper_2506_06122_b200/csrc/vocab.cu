@@ -410,7 +410,12 @@ bool use_tma(int esz) {
 // fused-loss pass: 1 = U4 + prefetch, 2 = U8, 3 = U2 + prefetch.
 template <typename ET, int NT, bool LOSS, bool ENT0, int MATH>
 cudaError_t launch_ldg_layout(const VocabArgs& a, int num_sms, cudaStream_t s) {
-  if constexpr (sizeof(ET) == 2 && NT == 3 && LOSS) {
+  if constexpr (sizeof(ET) == 2 && (MATH & kMathLazy)) {
+    // lazy max: software prefetch (U4 + the next batch in flight) measured +2% on cfg3
+    const int l = env_int("RLO_VOCAB_LDG", 1);
+    if (l == 1) return launch_ldg<ET, NT, LOSS, ENT0, MATH, 4, true>(a, num_sms, s);
+    if (NT == 3 && LOSS && l == 2) return launch_ldg<ET, NT, LOSS, ENT0, MATH, 8, false>(a, num_sms, s);
+  } else if constexpr (sizeof(ET) == 2 && NT == 3 && LOSS) {
     switch (env_int("RLO_VOCAB_LDG", 0)) {
       case 1: return launch_ldg<ET, NT, LOSS, ENT0, MATH, 4, true>(a, num_sms, s);
       case 2: return launch_ldg<ET, NT, LOSS, ENT0, MATH, 8, false>(a, num_sms, s);
@@ -431,11 +436,12 @@ cudaError_t launch_impl(const VocabArgs& a, int num_sms, cudaStream_t s) {
   return launch_ldg_layout<ET, NT, LOSS, ENT0, MATH>(a, num_sms, s);
 }
 
-// Instruction mix (vocab_common.cuh): fp32 {0, 1}, default 1; bf16 {1..6}, default 6 (profiles/r1_vocab_sweep.txt).
+// Instruction mix (vocab_common.cuh): fp32 {0, 1, 2 = 1 + lazy max}, default 1; bf16 {1..6, 7 = 6 + lazy
+// max, 8 = 1 + lazy max}, default 7 with the U4 + prefetch layout (profiles/r1_vocab_sweep.txt).
 template <typename ET, int NT, bool LOSS, bool ENT0>
 cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
   if ((int64_t)a.B * a.T == 0) return cudaSuccess;
-  const int math = env_int("RLO_VOCAB_MATH", sizeof(ET) == 2 ? 6 : 1);
+  const int math = env_int("RLO_VOCAB_MATH", sizeof(ET) == 2 ? 7 : 1);
   if constexpr (sizeof(ET) == 4) {
     return math == 0   ? launch_impl<ET, NT, LOSS, ENT0, 0>(a, num_sms, s)
            : math == 2 ? launch_impl<ET, NT, LOSS, ENT0, 1 | kMathLazy>(a, num_sms, s)
