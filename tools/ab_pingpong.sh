@@ -1,0 +1,10 @@
+# bf16 prefetch layout: ping-pong buffers (default) vs copy-forward (librlo_pfcopy.so); mix 7 vs 8 (no poly offload).
+set -u
+RLO_VOCAB_MATH=8 timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -1
+one() {  # $1 lib $2 math $3 config
+  RLO_LIB=$1 RLO_VOCAB_MATH=$2 timeout 600 python bench.py --config $3 --steps 3 --no-cpu-baseline --no-e2e 2>/dev/null | \
+    python -c "import sys,json; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); r=d['roofline']; p=d['p1']; print('lib=${1##*/} math=$2 cfg$3 P3', round(r['avg_launch_ms'],3), 'ms', round(r['achieved']), 'GB/s | P1', round(p['avg_launch_ms'],3), 'ms', round(p['achieved_gbs']), 'GB/s |', d['clocks']['sm_mhz'], 'MHz')"
+}
+for round in 1 2 3; do
+  one "" 7 3; one paper_2506_06122_b200/lib/variants/librlo_pfcopy.so 7 3; one "" 8 3
+done
