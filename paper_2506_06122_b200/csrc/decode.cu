@@ -206,19 +206,64 @@ __device__ __forceinline__ uint4 load_raw(const ET* z, int v, int lim, bool vec_
   return v < lim ? RawVec<ET>::fill(z, v, lim) : RawVec<ET>::fill(z, lim, lim);
 }
 
-// fp32 sum of the E weights 2^(x*c - mo) of one vector (3-level tree), in fp64.
+// fp32 sum of the E weights 2^(x*c - mo) of one vector, in fp64: packed
+// FFMA2 per element pair, MUFU.EX2 per element, a pairwise FADD2 tree (at
+// most 3 roundings deep, the bound screen_margin uses).
 template <typename ET>
 __device__ __forceinline__ double vec_wsum(const uint4& r, float c, float mo) {
   constexpr int E = RawVec<ET>::E;
-  float w[8];
+  const f2 c2 = pk2(c, c), m2 = pk2(-mo, -mo);
+  f2 acc[2];
 #pragma unroll
-  for (int e = 0; e < E; ++e) w[e] = ex2(fmaf(RawVec<ET>::at(r, e), c, -mo));  // -inf -> 0
-#pragma unroll
-  for (int h = E / 2; h > 0; h >>= 1) {
-#pragma unroll
-    for (int e = 0; e < h; ++e) w[e] += w[e + h];
+  for (int p = 0; p < E / 2; ++p) {
+    const f2 t = ffma2(pk2(RawVec<ET>::at(r, 2 * p), RawVec<ET>::at(r, 2 * p + 1)), c2, m2);
+    float tl, th;
+    upk2(t, tl, th);
+    const f2 e = pk2(ex2(tl), ex2(th));  // -inf -> 0
+    acc[p & 1] = p < 2 ? e : fadd2(acc[p & 1], e);
   }
-  return (double)w[0];
+  float lo, hi;
+  upk2(fadd2(acc[0], acc[1]), lo, hi);
+  return (double)(lo + hi);
+}
+
+// Largest of the U vectors' logits (packed bf16x2 max for bf16; exact).
+template <typename ET, int U>
+__device__ __forceinline__ float raw_max(const uint4 (&r)[U]) {
+  if constexpr (sizeof(ET) == 2) {
+    auto b2 = [](uint32_t x) { return *reinterpret_cast<__nv_bfloat162*>(&x); };
+    __nv_bfloat162 m = __hmax2(__hmax2(b2(r[0].x), b2(r[0].y)), __hmax2(b2(r[0].z), b2(r[0].w)));
+#pragma unroll
+    for (int k = 1; k < U; ++k) m = __hmax2(m, __hmax2(__hmax2(b2(r[k].x), b2(r[k].y)), __hmax2(b2(r[k].z), b2(r[k].w))));
+    return fmaxf(__low2float(m), __high2float(m));
+  } else {
+    float m = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      m = fmaxf(m, fmaxf(fmaxf(__uint_as_float(r[k].x), __uint_as_float(r[k].y)),
+                         fmaxf(__uint_as_float(r[k].z), __uint_as_float(r[k].w))));
+    return m;
+  }
+}
+
+// As vec_wsum, half of the element pairs through the FMA-pipe degree-4 exp2
+// (relative error 2.9e-6 per term, t clamped to its normal-range domain):
+// the untempered sum at T != 1, which only feeds the returned log-prob
+// (|lse error| <= 1.5e-6), so the MUFU pipe carries 1.5 instead of 2
+// exponentials per element there.  Never used for the certified weights.
+template <typename ET>
+__device__ __forceinline__ double vec_wsum_half_poly(const uint4& r, float c, float mo) {
+  constexpr int E = RawVec<ET>::E;
+  f2 acc = pk2(0.f, 0.f);
+#pragma unroll
+  for (int p = 0; p < E / 2; ++p) {
+    const float tl = fmaf(RawVec<ET>::at(r, 2 * p), c, -mo), th = fmaf(RawVec<ET>::at(r, 2 * p + 1), c, -mo);
+    const f2 e = (p & 1) ? exp2_poly2<4>(fmaxf(tl, -126.f), fmaxf(th, -126.f)) : pk2(ex2(tl), ex2(th));
+    acc = fadd2(acc, e);
+  }
+  float lo, hi;
+  upk2(acc, lo, hi);
+  return (double)(lo + hi);
 }
 
 // The screened fp32 path for one row (every thread of the CTA calls it; the
@@ -250,11 +295,7 @@ __device__ __forceinline__ bool screened_row(const ET* __restrict__ z, int V, in
     uint4 r[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) r[k] = load_raw<ET>(z, b + k * S, v1, vec_ok);
-    float cm = -INFINITY;
-#pragma unroll
-    for (int k = 0; k < U; ++k)
-#pragma unroll
-      for (int e = 0; e < E; ++e) cm = fmaxf(cm, RawVec<ET>::at(r[k], e));
+    const float cm = raw_max<ET, U>(r);
     if (cm > m) {
       const float nL = __fmul_rn(cm, kL2E), nT = unit_t ? nL : __fmul_rn(cm, cT);
       su *= exp2((double)mL - (double)nL);
@@ -264,9 +305,14 @@ __device__ __forceinline__ bool screened_row(const ET* __restrict__ z, int V, in
     if (m == -INFINITY) continue;
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      const double qs = vec_wsum<ET>(r[k], kL2E, mL);
-      su += qs;
-      st += unit_t ? qs : vec_wsum<ET>(r[k], cT, mT);
+      if (unit_t) {  // one set of weights, certified precision
+        const double qs = vec_wsum<ET>(r[k], kL2E, mL);
+        su += qs;
+        st += qs;
+      } else {
+        su += vec_wsum_half_poly<ET>(r[k], kL2E, mL);
+        st += vec_wsum<ET>(r[k], cT, mT);
+      }
     }
   }
 #pragma unroll
