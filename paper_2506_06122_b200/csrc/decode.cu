@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   __shared__ double tab[kExpTab];
   __shared__ double s_t[kDecWarps];
   __shared__ float s_m[kDecWarps], s_ml[kDecWarps], s_su[kDecWarps];
-  __shared__ double s_base, s_thresh, s_lse, s_total;
+  __shared__ double s_base, s_thresh, s_lse;
   __shared__ float s_M;
   __shared__ int s_warp, s_pick;
 
