@@ -236,10 +236,11 @@ def run_ours(args, c):
     ms = t0.elapsed_time(t1)
     vk = [a.elapsed_time(b) for a, b in vocab_ms]
     vocab_avg_ms = float(np.mean(vk))
+    vocab_avg_ms_slowest = vocab_avg_ms
     if dist:
-        tt = torch.tensor([ms], device=dev)
+        tt = torch.tensor([ms, vocab_avg_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+        ms, vocab_avg_ms_slowest = float(tt[0].item()), float(tt[1].item())
 
     # ---- P=1: actor-only pass, old/ref log-probs precomputed ----
     p1 = None if args.no_p1 else run_p1(args, c, obj, rlo, torch, cfg, logits, tokens, dside, adv, logp, stream,
@@ -273,7 +274,8 @@ def run_ours(args, c):
                      "traffic": traffic_from_profile(args.config), "peak_kind": peak_kind,
                      "frac_of_spec_8000": achieved / 8000.0,
                      "kernel": "vocab_kernel (fused 3-tensor logprob+entropy+loss pass, incl. per-seq reduce)",
-                     "bytes_per_launch": bytes_per_launch, "avg_launch_ms": vocab_avg_ms},
+                     "bytes_per_launch": bytes_per_launch, "avg_launch_ms": vocab_avg_ms,
+                     **({"avg_launch_ms_slowest_rank": vocab_avg_ms_slowest} if world > 1 else {})},
         "e2e": e2e,
         "p1": p1,
         "gpu_launches": launches,
