@@ -405,6 +405,8 @@ bool use_tma(int esz) {
   return false;  // default: LDG streaming (measured faster than the TMA ring for fp32 and bf16, profiles/)
 }
 
+constexpr int kLongRowV = 65536;  // bf16 rows of >= 128 KB count as long
+
 // LDG layout per dtype: fp32 U=8 (128 B in flight per thread); bf16 U=4
 // (64 B).  RLO_VOCAB_LDG selects the alternatives compiled for the hot bf16
 // fused-loss pass: 1 = U4 + prefetch, 2 = U8, 3 = U2 + prefetch.
@@ -416,7 +418,7 @@ cudaError_t launch_ldg_layout(const VocabArgs& a, int num_sms, cudaStream_t s) {
     if (l == 1) return launch_ldg<ET, NT, LOSS, ENT0, MATH, 4, true>(a, num_sms, s);
     if (NT == 3 && LOSS && l == 2) return launch_ldg<ET, NT, LOSS, ENT0, MATH, 8, false>(a, num_sms, s);
   } else if constexpr (sizeof(ET) == 2 && NT == 3 && LOSS) {
-    switch (env_int("RLO_VOCAB_LDG", 0)) {
+    switch (env_int("RLO_VOCAB_LDG", a.V < kLongRowV ? 4 : 0)) {  // short rows: lockstep streams
       case 1: return launch_ldg<ET, NT, LOSS, ENT0, MATH, 4, true>(a, num_sms, s);
       case 2: return launch_ldg<ET, NT, LOSS, ENT0, MATH, 8, false>(a, num_sms, s);
       case 3: return launch_ldg<ET, NT, LOSS, ENT0, MATH, 2, true>(a, num_sms, s);
@@ -441,7 +443,11 @@ cudaError_t launch_impl(const VocabArgs& a, int num_sms, cudaStream_t s) {
 template <typename ET, int NT, bool LOSS, bool ENT0>
 cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
   if ((int64_t)a.B * a.T == 0) return cudaSuccess;
-  const int math = env_int("RLO_VOCAB_MATH", sizeof(ET) == 2 ? 7 : 1);
+  // bf16: the lazy max + prefetch (mix 7), except the 3-tensor loss pass over
+  // short rows (< 128 KB), which takes mix 6 with lockstep streams (per-row
+  // cold starts dominate there; profiles/r1_vocab_sweep.txt)
+  const bool short3 = NT == 3 && LOSS && a.V < kLongRowV;
+  const int math = env_int("RLO_VOCAB_MATH", sizeof(ET) == 2 ? (short3 ? 6 : 7) : 1);
   if constexpr (sizeof(ET) == 4) {
     return math == 0   ? launch_impl<ET, NT, LOSS, ENT0, 0>(a, num_sms, s)
            : math == 2 ? launch_impl<ET, NT, LOSS, ENT0, 1 | kMathLazy>(a, num_sms, s)
