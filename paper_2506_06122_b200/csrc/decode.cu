@@ -15,26 +15,29 @@
 //
 // Two paths per row.  The screened fp32 path (default) computes the tempered
 // weights 2^(z*cT - mT) with MUFU.EX2 in fp32 (vector sums of 4-8 accumulated
-// in fp64), walks the CDF the same way, and accepts its pick only with a
-// certificate: the threshold X = u * total lies more than margin * total
-// inside the picked token's CDF interval, margin = 2.5 x eps(V), where eps(V)
-// bounds the error of every fp32-derived CDF value and of X relative to the
-// total (screen_margin below):
-//   argument rounding, |dt| <= |t| 2^-24 per term, and the fp32 constant
-//   cT = log2(e)/T, |dt| <= |t| 2^-24: sum_v w_v |t_v| ln2 2^-24 each, and
-//   sum_v w_v |t_v| <= total * log2(V) (sum p (-log2 p) <= log2 V, the max
-//   weight being 1);
-//   ex2.approx.ftz.f32 <= 1.44e-7 relative (exhaustive over t in [-126, 1] on
-//   B200, tools/probes/ex2_probe.cu; 1.5e-7 used); the fp32 vector tree
-//   <= 3 * 2^-24; fp64 accumulation and the fp64 rescales negligible.
+// in fp64), walks the CDF the same way, and accepts its pick c only with a
+// certificate: X = u * total lies more than margin * total inside
+// (CDF(c-1), CDF(c)].  Every element enters the total, the CDF and X through
+// ONE computed weight w^_v, so the error of X - CDF(c-1) is
+// (u - 1) sum_{v<c} (w^_v - w_v) + u sum_{v>=c} (w^_v - w_v), at most
+// max(u, 1-u) * eps_e * total (likewise CDF(c) - X), where
+//   eps_e * total >= sum_v |w^_v - w_v|: argument rounding |dt| <= |t| 2^-24
+//   and the fp32 constant cT = log2(e)/T, |dt| <= |t| 2^-24, give
+//   2^-24 ln2 sum_v w_v |t_v| each, and sum_v w_v |t_v| <= total * log2(V)
+//   (sum p (-log2 p) <= log2 V, the max weight being 1); ex2.approx.ftz.f32
+//   <= 1.44e-7 relative (exhaustive over t in [-126, 1] on B200,
+//   tools/probes/ex2_probe.cu; 1.5e-7 used);
+// plus the two summation orders (kScreenSum = 2 x a 3-deep fp32 tree; fp64
+// accumulation and the fp64 rescales negligible):
+//   margin = 1.1 * (max(u, 1-u) * eps_e(V) + kScreenSum), 0.9-1.6e-6 at V = 152064.
 // Under the certificate the exact CDF walk picks the same token, so the draw
 // is the fp64 path's.  A row without one (a CDF boundary within the margin,
-// most likely on flat rows: 5-23% of synthetic Qwen-vocabulary draws at
-// T = 0.6-1.0, profiles/r1_next_rows.txt; or non-finite sums) is redone by the
-// fp64 path — the weights exp((z - m)/T) in fp64 through a table-driven exp
-// (exp_neg), bound by fp64 throughput (~13 fp64 operations per element) — in
-// a second launch that skips the certified rows.  RLO_DECODE_MARGIN overrides
-// the margin (<= 0: fp64 path only; >= 1: every row redone, for tests).
+// most likely on flat rows, profiles/r1_next_rows.txt; or non-finite sums) is
+// redone by the fp64 path — the weights exp((z - m)/T) in fp64 through a
+// table-driven exp (exp_neg), bound by fp64 throughput (~13 fp64 operations
+// per element) — in a second launch that skips the certified rows.
+// RLO_DECODE_MARGIN fixes the margin instead (<= 0: fp64 path only; >= 1:
+// every row redone, for tests).
 #include <cuda_bf16.h>
 
 #include <cmath>
@@ -144,12 +147,17 @@ __device__ __forceinline__ void load_e(const ET* z, int v, int lim, bool vec_ok,
   }
 }
 
-// The certificate margin (relative to the total) for a vocabulary of V tokens.
-inline double screen_margin(int V) {
-  const double u = 0x1p-24;
-  const double eps = 2.0 * std::log2((double)(V > 2 ? V : 2)) * u * 0.6931471805599453 + 1.5e-7 + 3.0 * u;
-  return 2.5 * eps;
+// The certificate's error terms, relative to the total, for a vocabulary of
+// V tokens: eps_e bounds sum_v |w^_v - w_v| (argument rounding and the fp32
+// log2(e)/T constant, 2^-24 ln2 sum w|t| each with sum w|t| <= total log2 V;
+// ex2.approx 1.5e-7), kScreenSum the summation of two differently grouped
+// sums (2 x a 3-deep fp32 tree; fp64 accumulation negligible).
+inline double screen_eps(int V) {
+  return 2.0 * std::log2((double)(V > 2 ? V : 2)) * 0x1p-24 * 0.6931471805599453 + 1.5e-7;
 }
+constexpr double kScreenSum = 6.0 * 0x1p-24;
+constexpr double kScreenSafety = 1.1;  // second-order terms
+
 #ifndef RLO_SCREEN_U
 #define RLO_SCREEN_U 4
 #endif
@@ -208,7 +216,7 @@ __device__ __forceinline__ uint4 load_raw(const ET* z, int v, int lim, bool vec_
 
 // fp32 sum of the E weights 2^(x*c - mo) of one vector, in fp64: packed
 // FFMA2 per element pair, MUFU.EX2 per element, a pairwise FADD2 tree (at
-// most 3 roundings deep, the bound screen_margin uses).
+// most 3 roundings deep, the bound kScreenSum uses).
 template <typename ET>
 __device__ __forceinline__ double vec_wsum(const uint4& r, float c, float mo) {
   constexpr int E = RawVec<ET>::E;
@@ -278,12 +286,14 @@ __device__ __forceinline__ double vec_wsum_half_poly(const uint4& r, float c, fl
 //           (kScreenU steps in flight per warp) into shared memory;
 //   warp 0: scans the step sums for the crossing step, walks it (warp prefix
 //           of the lane sums, then the hit lane's tokens in order) and checks
-//           the certificate X - CDF(c-1) > margin * total, CDF(c) - X > margin * total.
+//           the certificate X - CDF(c-1) > margin * total, CDF(c) - X > margin * total
+//           (total and X re-formed with the step sums, see the header).
 // Returns true with s_pick / s_lse set when the certificate holds; false
 // sends the row to the fp64 path.
 template <typename ET>
 __device__ __forceinline__ bool screened_row(const ET* __restrict__ z, int V, int W, bool vec_ok, bool unit_t, float cT,
-                                             double margin, double u, double* s_t, double* s_u2, float* s_mt,
+                                             double eps_e, double fixed, double u, double* s_t, double* s_u2,
+                                             float* s_mt,
                                              float* s_ml, double* s_step, double& s_thresh, double& s_total,
                                              double& s_lse, int& s_warp, int& s_pick, int& s_ok) {
   constexpr int E = RawVec<ET>::E, S = 32 * E, U = kScreenU;
@@ -335,7 +345,8 @@ __device__ __forceinline__ bool screened_row(const ET* __restrict__ z, int V, in
       T += s_t[j];
       Uu += s_u2[j] * exp2((double)s_ml[j] - ML);
     }
-    const double X = u * T, mg = margin * T;
+    // worst-case margin for the early outs (u-dependent certificate below)
+    const double X = u * T, mg = (fixed > 0.0 ? fixed : kScreenSafety * (eps_e + kScreenSum)) * T;
     int jw = -1;
     double base = 0.0;
     // a threshold within the margin of the total (the reference's no-crossing
@@ -350,7 +361,8 @@ __device__ __forceinline__ bool screened_row(const ET* __restrict__ z, int V, in
       }
     }
     s_warp = jw;
-    s_u2[0] = base;  // CDF before the crossing warp range
+    s_u2[0] = base;  // CDF before the crossing warp range (pass-1 sums)
+    s_u2[1] = jw >= 0 ? T - s_t[jw] : 0.0;  // pass-1 mass outside it
     s_thresh = X;
     s_total = T;
     s_mt[0] = MT;
@@ -377,7 +389,18 @@ __device__ __forceinline__ bool screened_row(const ET* __restrict__ z, int V, in
   }
   __syncthreads();
   if (warp == 0) {
-    const double X = s_thresh, mg = margin * s_total;
+    // One computed weight per element from here on: the total is re-formed
+    // from the pass-1 sums outside the crossing range and the step sums
+    // inside it (the walk's weights are bitwise those of the step sums), so
+    // with X = u * total the errors of X - CDF(c-1) and CDF(c) - X are
+    // (u - 1) e_before + u e_after: at most max(u, 1 - u) * eps_e * total,
+    // plus the two summation orders.
+    double td = 0.0;
+    for (int c = lane; c < nsteps; c += 32) td += s_step[c];
+    td = warp_sum(td);
+    const double T2 = s_u2[1] + td;
+    const double X = u * T2;
+    const double mg = (fixed > 0.0 ? fixed : kScreenSafety * (fmax(u, 1.0 - u) * eps_e + kScreenSum)) * T2;
     double base = s_u2[0];
     int ks = -1;
     for (int c = 0; c < nsteps && ks < 0; c += 32) {  // first step whose inclusive CDF passes X
@@ -665,7 +688,7 @@ template <typename ET>
 __global__ void __launch_bounds__(kDecWarps * 32, RLO_SCREEN_MINB)
     decode_screen_kernel(const ET* __restrict__ logits, int64_t stride, int V, int n, double temp, uint64_t seed,
                          uint64_t version, const uint64_t* __restrict__ keys, const uint64_t* __restrict__ positions,
-                         int32_t* __restrict__ out_tok, float* __restrict__ out_lp, double margin) {
+                         int32_t* __restrict__ out_tok, float* __restrict__ out_lp, double eps_e, double fixed) {
   constexpr int E = RawVec<ET>::E;
   __shared__ double s_t[kDecWarps], s_u2[kDecWarps];
   __shared__ double s_step[kStepMax];
@@ -678,7 +701,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, RLO_SCREEN_MINB)
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(logits) & 15u) == 0) && (((stride * (int64_t)sizeof(ET)) & 15) == 0);
   for (int row = blockIdx.x; row < n; row += gridDim.x) {
     const ET* z = logits + (int64_t)row * stride;
-    const bool ok = screened_row<ET>(z, V, W, vec_ok, unit_t, cT, margin,
+    const bool ok = screened_row<ET>(z, V, W, vec_ok, unit_t, cT, eps_e, fixed,
                                      keyed_double4(seed, version, keys[row], positions[row]), s_t, s_u2, s_mt, s_ml,
                                      s_step, s_thresh, s_total, s_lse, s_warp, s_pick, s_ok);
     if (threadIdx.x == 0) {
@@ -697,20 +720,23 @@ cudaError_t launch_decode(const void* logits, int32_t dtype, int64_t stride, int
   if (n == 0) return cudaSuccess;
   const int grid = n < num_sms * 8 ? n : num_sms * 8;
   const char* me = std::getenv("RLO_DECODE_MARGIN");
-  const double margin = (me && *me) ? std::atof(me) : screen_margin(V);
+  // RLO_DECODE_MARGIN: a fixed margin instead of the derived one (<= 0: no screen)
+  const double fixed = (me && *me) ? std::atof(me) : -1.0;
+  const double eps_e = screen_eps(V);
+  const bool screen = !(me && *me) || fixed > 0.0;
   const bool bf = dtype == RLO_DTYPE_BF16;
-  if (margin > 0.0) {
+  if (screen) {
     if (bf)
       decode_screen_kernel<__nv_bfloat16><<<grid, kDecWarps * 32, 0, s>>>(
           reinterpret_cast<const __nv_bfloat16*>(logits), stride, V, n, temperature, seed, version, keys, positions,
-          out_tok, out_lp, margin);
+          out_tok, out_lp, eps_e, fixed);
     else
       decode_screen_kernel<float><<<grid, kDecWarps * 32, 0, s>>>(reinterpret_cast<const float*>(logits), stride, V,
                                                                   n, temperature, seed, version, keys, positions,
-                                                                  out_tok, out_lp, margin);
+                                                                  out_tok, out_lp, eps_e, fixed);
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
-  const bool redo = margin > 0.0;  // the fp64 kernel redoes only the rows the screen left (out_tok = -1)
+  const bool redo = screen;  // the fp64 kernel redoes only the rows the screen left (out_tok = -1)
   const char* nr = std::getenv("RLO_DECODE_NOREDO");  // diagnostics: leave the screen's -1 marks (fail rate)
   if (redo && nr && *nr == '1') return cudaGetLastError();
   if (bf)
