@@ -336,38 +336,42 @@ __device__ __forceinline__ bool screened_row(const ET* __restrict__ z, int V, in
   }
   if (lane == 0) s_t[warp] = st, s_u2[warp] = su, s_mt[warp] = mT, s_ml[warp] = mL;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float MT = s_mt[0], ML = s_ml[0];
-    for (int j = 1; j < kDecWarps; ++j) MT = fmaxf(MT, s_mt[j]), ML = fmaxf(ML, s_ml[j]);
-    double T = 0.0, Uu = 0.0;
-    for (int j = 0; j < kDecWarps; ++j) {
-      s_t[j] *= exp2((double)s_mt[j] - MT);
-      T += s_t[j];
-      Uu += s_u2[j] * exp2((double)s_ml[j] - ML);
+  if (warp == 0) {  // combine the 8 warp states: lanes 0-7 in parallel
+    const bool in = lane < kDecWarps;
+    float MT = in ? s_mt[lane] : -INFINITY, ML = in ? s_ml[lane] : -INFINITY;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      MT = fmaxf(MT, __shfl_xor_sync(0xffffffffu, MT, o));
+      ML = fmaxf(ML, __shfl_xor_sync(0xffffffffu, ML, o));
     }
+    const double tj = in ? s_t[lane] * exp2((double)s_mt[lane] - MT) : 0.0;
+    const double T = warp_sum(tj);
+    const double Uu = warp_sum(in ? s_u2[lane] * exp2((double)s_ml[lane] - ML) : 0.0);
     // worst-case margin for the early outs (u-dependent certificate below)
     const double X = u * T, mg = (fixed > 0.0 ? fixed : kScreenSafety * (eps_e + kScreenSum)) * T;
-    int jw = -1;
-    double base = 0.0;
+    double incl = tj;  // inclusive prefix of the warp sums in token order
+#pragma unroll
+    for (int o = 1; o < kDecWarps; o <<= 1) {
+      const double q = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += q;
+    }
     // a threshold within the margin of the total (the reference's no-crossing
     // fallback to the last token is in play) or non-finite sums: fp64 path
-    if (isfinite(T) && T > 0.0 && isfinite(Uu) && Uu > 0.0 && X < T - mg && W / S <= kStepMax) {
-      for (int j = 0; j < kDecWarps; ++j) {
-        if (X < base + s_t[j]) {
-          jw = j;
-          break;
-        }
-        base += s_t[j];
-      }
+    const bool go = isfinite(T) && T > 0.0 && isfinite(Uu) && Uu > 0.0 && X < T - mg && W / S <= kStepMax;
+    const unsigned hit = __ballot_sync(0xffffffffu, go && in && X < incl);
+    const int jw = hit ? __ffs(hit) - 1 : -1;
+    const double base = jw >= 0 ? __shfl_sync(0xffffffffu, incl - tj, jw) : 0.0;
+    const double tw = jw >= 0 ? __shfl_sync(0xffffffffu, tj, jw) : 0.0;
+    if (lane == 0) {
+      s_warp = jw;
+      s_u2[0] = base;                       // CDF before the crossing warp range (pass-1 sums)
+      s_u2[1] = jw >= 0 ? T - tw : 0.0;     // pass-1 mass outside it
+      s_thresh = X;
+      s_total = T;
+      s_mt[0] = MT;
+      s_lse = ((double)ML + log2(Uu)) / (double)kL2E;
+      s_ok = 0;
     }
-    s_warp = jw;
-    s_u2[0] = base;  // CDF before the crossing warp range (pass-1 sums)
-    s_u2[1] = jw >= 0 ? T - s_t[jw] : 0.0;  // pass-1 mass outside it
-    s_thresh = X;
-    s_total = T;
-    s_mt[0] = MT;
-    s_lse = ((double)ML + log2(Uu)) / (double)kL2E;
-    s_ok = 0;
   }
   __syncthreads();
   const int jw = s_warp;
