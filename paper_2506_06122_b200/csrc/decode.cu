@@ -326,12 +326,15 @@ __device__ __forceinline__ bool screened_row(const ET* __restrict__ z, int V, in
     }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float ml2 = __shfl_xor_sync(0xffffffffu, mL, o), mt2 = __shfl_xor_sync(0xffffffffu, mT, o);
-    const double su2 = __shfl_xor_sync(0xffffffffu, su, o), st2 = __shfl_xor_sync(0xffffffffu, st, o);
-    const float ML = fmaxf(mL, ml2), MT = fmaxf(mT, mt2);
-    su = su * exp2((double)mL - ML) + su2 * exp2((double)ml2 - ML);
-    st = st * exp2((double)mT - MT) + st2 * exp2((double)mt2 - MT);
+  {  // warp combine: the warp's max first, then one fp64 rescale per lane and plain sums
+    float ML = mL, MT = mT;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ML = fmaxf(ML, __shfl_xor_sync(0xffffffffu, ML, o));
+      MT = fmaxf(MT, __shfl_xor_sync(0xffffffffu, MT, o));
+    }
+    su = warp_sum(su * exp2((double)mL - ML));
+    st = warp_sum(st * exp2((double)mT - MT));
     mL = ML, mT = MT;
   }
   if (lane == 0) s_t[warp] = st, s_u2[warp] = su, s_mt[warp] = mT, s_ml[warp] = mL;
@@ -534,18 +537,15 @@ __global__ void __launch_bounds__(kDecWarps * 32)
       su += q[0];
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {  // warp combine (max, rescaled sums)
-      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
-      const double t2 = __shfl_xor_sync(0xffffffffu, st, o);
-      const float ml2 = __shfl_xor_sync(0xffffffffu, mL, o);
-      const float u2 = __shfl_xor_sync(0xffffffffu, su, o);
-      const float M = fmaxf(m, m2);
-      if (M != -INFINITY) {
-        st = (m == -INFINITY ? 0.0 : st * exp_neg(unit_t ? (double)m - M : ((double)m - M) * inv_t, tab)) +
-             (m2 == -INFINITY ? 0.0 : t2 * exp_neg(unit_t ? (double)m2 - M : ((double)m2 - M) * inv_t, tab));
+    {  // warp combine: the warp's max first, then one rescale per lane and plain sums
+      float M = m, ML = mL;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        ML = fmaxf(ML, __shfl_xor_sync(0xffffffffu, ML, o));
       }
-      const float ML = fmaxf(mL, ml2);
-      su = su * ex2(mL - ML) + u2 * ex2(ml2 - ML);
+      st = warp_sum(m == -INFINITY ? 0.0 : st * exp_neg(unit_t ? (double)m - M : ((double)m - M) * inv_t, tab));
+      su = warp_sum(su * ex2(mL - ML));
       m = M;
       mL = ML;
     }
