@@ -65,15 +65,39 @@ __device__ __forceinline__ void acc_combine(Acc& a, float mL2, float s2, float w
   a.mL = M;
 }
 
+#ifndef RLO_WARP_REDUCE_PAIRWISE
+#define RLO_WARP_REDUCE_PAIRWISE 0
+#endif
+// Warp reduction of the online state: the warp's max first (5 FMNMX
+// shuffles), then one rescale per lane and plain shuffle sums — one EX2 per
+// lane instead of two per level (RLO_WARP_REDUCE_PAIRWISE=1: the pairwise
+// combine at every level, kept for A/B).
 template <bool ENT>
 __device__ __forceinline__ void acc_warp_reduce(Acc& a) {
+  if (RLO_WARP_REDUCE_PAIRWISE) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, a.mL, o);
+      const float s2 = __shfl_xor_sync(0xffffffffu, a.s, o);
+      const float w2 = ENT ? __shfl_xor_sync(0xffffffffu, a.w, o) : 0.f;
+      acc_combine<ENT>(a, m2, s2, w2);
+    }
+    return;
+  }
+  float M = a.mL;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  const float d = a.mL - M, sc = ex2(d);
+  float s = a.s * sc, w = 0.f;
+  if (ENT) w = (a.w + a.s * d) * sc;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    const float m2 = __shfl_xor_sync(0xffffffffu, a.mL, o);
-    const float s2 = __shfl_xor_sync(0xffffffffu, a.s, o);
-    const float w2 = ENT ? __shfl_xor_sync(0xffffffffu, a.w, o) : 0.f;
-    acc_combine<ENT>(a, m2, s2, w2);
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (ENT) w += __shfl_xor_sync(0xffffffffu, w, o);
   }
+  a.mL = M;
+  a.s = s;
+  if (ENT) a.w = w;
 }
 
 // ---- per-dtype 16-byte vector math -------------------------------------------
