@@ -161,6 +161,9 @@ constexpr double kScreenSafety = 1.1;  // second-order terms
 #ifndef RLO_SCREEN_U
 #define RLO_SCREEN_U 4
 #endif
+#ifndef RLO_SCREEN_POLY  // untempered exponentials on the FMA pipe: 0 none, 1 half (default), 2 all
+#define RLO_SCREEN_POLY 1
+#endif
 #ifndef RLO_SCREEN_MINB
 #define RLO_SCREEN_MINB 4
 #endif
@@ -266,7 +269,8 @@ __device__ __forceinline__ double vec_wsum_half_poly(const uint4& r, float c, fl
 #pragma unroll
   for (int p = 0; p < E / 2; ++p) {
     const float tl = fmaf(RawVec<ET>::at(r, 2 * p), c, -mo), th = fmaf(RawVec<ET>::at(r, 2 * p + 1), c, -mo);
-    const f2 e = (p & 1) ? exp2_poly2<4>(fmaxf(tl, -126.f), fmaxf(th, -126.f)) : pk2(ex2(tl), ex2(th));
+    const bool poly = RLO_SCREEN_POLY == 2 ? true : RLO_SCREEN_POLY == 1 ? (p & 1) != 0 : false;
+    const f2 e = poly ? exp2_poly2<4>(fmaxf(tl, -126.f), fmaxf(th, -126.f)) : pk2(ex2(tl), ex2(th));
     acc = fadd2(acc, e);
   }
   float lo, hi;
