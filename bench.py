@@ -242,6 +242,12 @@ def run_ours(args, c):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms, vocab_avg_ms_slowest = float(tt[0].item()), float(tt[1].item())
 
+    nrow = B * T  # sampled results of the last timed step (checked in the CPU leg)
+    sample_rows = sorted({0, nrow - 1, key_rows - 1, min(key_rows, nrow - 1), nrow // 2, (7 * nrow) // 11,
+                          12345 % nrow})
+    lp_sample = logp.view(-1)[torch.tensor(sample_rows, device=dev)].cpu().numpy()
+    tok_sample = tokens.view(-1)[torch.tensor(sample_rows, device=dev)].cpu().numpy()
+
     # ---- P=1: actor-only pass, old/ref log-probs precomputed ----
     p1 = None if args.no_p1 else run_p1(args, c, obj, rlo, torch, cfg, logits, tokens, dside, adv, logp, stream,
                                        barrier, dist, mb, esz)
@@ -251,6 +257,7 @@ def run_ours(args, c):
                                            key_rows, mb)
 
     peak, peak_kind = load_peaks()
+    traffic = traffic_from_profile(args.config)
     tokens_per_step = B * T  # full-length responses, all positions loss-participating
     per_row_side = 4 + 4 + 17  # token id, advantage, per-token results written for the reduction
     bytes_per_launch = mb * T * (3 * V * esz + per_row_side)
@@ -271,7 +278,7 @@ def run_ours(args, c):
                          f"micro-batch vs 126 MB L2",
                    "parallelism": f"dp{world}"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic_from_profile(args.config), "peak_kind": peak_kind,
+                     "traffic": traffic[0], "traffic_source": traffic[1], "peak_kind": peak_kind,
                      "frac_of_spec_8000": achieved / 8000.0,
                      "kernel": "vocab_kernel (fused 3-tensor logprob+entropy+loss pass, incl. per-seq reduce)",
                      "bytes_per_launch": bytes_per_launch, "avg_launch_ms": vocab_avg_ms,
@@ -284,7 +291,11 @@ def run_ours(args, c):
                   "mean_kl": st.mean_kl, "tokens": st.tokens, "mean_entropy": st.mean_entropy},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(args, c, target_s=args.cpu_seconds)
+        # the last timed step's actor log-probs on a few sampled token rows, for
+        # the oracle check inside the CPU leg (row r reads resident logits row
+        # r mod key_rows; rank 0: token and logits keys coincide)
+        out["cpu_baseline"] = cpu_baseline(args, c, target_s=args.cpu_seconds,
+                                           check=(sample_rows, key_rows, lp_sample, tok_sample))
     obj.close()
     if dist:
         dist.destroy_process_group()
@@ -390,24 +401,19 @@ def run_e2e(args, c, obj, rlo, torch, cfg, logits, side, dev, stream, dist, key_
                                  ref_logits=logits[2], adv_out=adv_host.numpy(), logp_out=logp_host.numpy())
         api = "rlo_objective_step_host (C ABI, host buffers)"
     else:
-        d = {k: torch.empty_like(v, device=dev) for k, v in pin.items()}
-        tok_d = torch.empty(B, T, dtype=torch.int32, device=dev)
-        adv_d = torch.empty(B, T, dtype=torch.float32, device=dev)
-        logp_d = torch.empty(B, T, dtype=torch.float32, device=dev)
+        # micro-batched: the whole batch's host arrays go in once, the logits
+        # callback names each micro-batch's device logits (here the resident
+        # chunk, which a trainer's model forward would refill), results come back
+        def logits_fn(i, b0, nb):
+            return logits[0], logits[1], logits[2]
 
         def step():
-            for k in pin:
-                d[k].copy_(pin[k], non_blocking=True)
-            tok_d.copy_(tok_host, non_blocking=True)
-            obj.compute_advantages(cfg, d["lengths"], T=T, rewards=d.get("rewards"),
-                                   scalar_rewards=d.get("scalar_rewards"), values=d.get("values"), out=adv_d)
-            for i in range(B // mb):
-                s = slice(i * mb, (i + 1) * mb)
-                _ppo(obj, rlo, cfg, tok_d[s], d["lengths"][s], logits, adv_d[s], i * mb, logp_d[s])
-            adv_host.copy_(adv_d, non_blocking=True)
-            logp_host.copy_(logp_d, non_blocking=True)
-            return obj.merge_gradients(cfg)  # synchronises the stream
-        api = "Objective.compute_advantages/ppo_gradient/merge_gradients with pinned host I/O"
+            return obj.step_host_mb(cfg, tok_host.numpy(), pin["lengths"].numpy(), mb, logits_fn,
+                                    rewards=pin["rewards"].numpy() if "rewards" in pin else None,
+                                    scalar_rewards=pin["scalar_rewards"].numpy() if "scalar_rewards" in pin else None,
+                                    values=pin["values"].numpy() if "values" in pin else None,
+                                    adv_out=adv_host.numpy(), logp_out=logp_host.numpy())
+        api = "rlo_objective_step_host_mb (C ABI, host buffers, per-micro-batch logits callback)"
 
     for _ in range(max(1, args.warmup)):
         step()
@@ -428,21 +434,61 @@ def run_e2e(args, c, obj, rlo, torch, cfg, logits, side, dev, stream, dist, key_
             "d2h_bytes_per_step": hb_out + 64, "api": api, "ms_per_step": 1e3 * el / args.steps}
 
 
+def kernel_source_hash():
+    """sha256 over the CUDA sources of the library (csrc/*.cu, *.cuh, *.h):
+    identifies the kernels a stored ncu capture was taken from."""
+    import glob
+    import hashlib
+    h = hashlib.sha256()
+    src = os.path.join(ROOT, "paper_2506_06122_b200", "csrc")
+    for p in sorted(glob.glob(os.path.join(src, "*.cu")) + glob.glob(os.path.join(src, "*.cuh")) +
+                    glob.glob(os.path.join(src, "*.h"))):
+        with open(p, "rb") as f:
+            h.update(os.path.basename(p).encode() + b"\0" + f.read())
+    return h.hexdigest()[:16]
+
+
 def traffic_from_profile(cfg_id):
+    """DRAM bytes per launch of the vocab kernel from the committed ncu
+    capture (profiles/ncu_traffic.json, written by tools/ncu_traffic.py) --
+    used only when that capture was taken from the kernel sources this run
+    was built from (source hash match); otherwise null, never a stale value."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
-        return None
+        return None, "no capture"
     with open(p) as f:
         d = json.load(f)
     v = d.get(f"cfg{cfg_id}")
-    return None if v is None else v.get("bytes_per_launch")
+    if v is None:
+        return None, "no capture for this config"
+    if v.get("src_hash") != kernel_source_hash():
+        return None, "capture is from other kernel sources (stale): not used"
+    return v.get("bytes_per_launch"), f"ncu capture {v.get('capture', '')} (src {v.get('src_hash')})"
 
 
-def cpu_baseline(args, c, target_s=12.0, use_ref=None):
+def oracle_check(O, c, seed, check):
+    """The timed run's own results against the fp64 oracle: actor log-probs of
+    sampled token rows of the last timed step (|gpu - oracle| <= 1e-5 *
+    max(1, |oracle|), the north_star tolerance)."""
+    rows, key_rows, lp_gpu, toks = check
+    dt = O.F32 if c["dtype"] == "f32" else O.BF16
+    worst = 0.0
+    for r, g, tok in zip(rows, lp_gpu, toks):
+        z = O.synth_row(dt, c["V"], seed, 0, r % key_rows)
+        lse, _ = O.logsoftmax_row(z)
+        want = z[int(tok)] - lse
+        worst = max(worst, abs(float(g) - want) / max(1.0, abs(want)))
+    return {"rows": len(rows), "what": "actor logp of sampled rows of the last timed step vs oracle",
+            "max_scaled_err": worst, "tol": 1e-5, "ok": worst <= 1e-5}
+
+
+def cpu_baseline(args, c, target_s=12.0, use_ref=None, check=None):
     """The reference's CPU path (oracle/_ref: the reference's own
     next_token_forward log-softmax, compute_advantages, merge_gradients) on a
-    bounded sample of the same workload, all host threads."""
+    bounded sample of the same workload, all host threads.  With `check`, the
+    GPU run's sampled results are first checked against the oracle."""
     import oracle as O
+    chk_out = oracle_check(O, c, args.seed, check) if check is not None else None
     if use_ref is None:
         use_ref = O.ref_available()
     threads = os.cpu_count() or 1
@@ -465,7 +511,8 @@ def cpu_baseline(args, c, target_s=12.0, use_ref=None):
             "kind": "reference" if use_ref else "port",
             "sample": f"{Bs} seqs x {Ts} tokens of {c['name'].split(':')[0]} (V={V} {c['dtype']}, 3 logits "
                       f"passes via the reference's next_token_forward log-softmax, {key_rows} resident rows/model), "
-                      f"{secs:.1f} s", "seconds": secs, "checksum_loss": chk, "B_sample": Bs, "T_sample": Ts}
+                      f"{secs:.1f} s", "seconds": secs, "checksum_loss": chk, "B_sample": Bs, "T_sample": Ts,
+            **({"gpu_oracle_check": chk_out} if chk_out is not None else {})}
 
 
 def run_reference(args, c):
@@ -505,7 +552,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS),
+                    help="BASELINE.json config (default 3: the north_star's Qwen2.5-7B-vocab bf16 batch)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

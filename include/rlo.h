@@ -39,7 +39,7 @@ extern "C" {
 #pragma GCC visibility push(default) /* the library is built -fvisibility=hidden; export exactly this header */
 #endif
 
-#define RLO_ABI_VERSION 4
+#define RLO_ABI_VERSION 5
 
 /* Status codes — reference exception taxonomy (include/rollmini/errors.hpp). */
 typedef enum rlo_status {
@@ -322,6 +322,32 @@ rlo_status rlo_objective_step_host(rlo_handle* h, const rlo_train_config* cfg, i
                                    const float* old_logp, const float* ref_logp,
                                    float* host_adv_out, float* host_logp_out, rlo_stats* stats,
                                    void* stream);
+
+/* Micro-batched host-buffer step — the reference-facing call when the logits
+ * of the whole batch do not fit in HBM at once (Qwen-vocabulary batches:
+ * 1.3 TB per model for BASELINE cfg 3).  The SampleBatch arrays of all B
+ * sequences are in (preferably pinned) host memory and are copied to the
+ * device once; advantages (with the global whitening statistics) are computed
+ * over the whole batch; then for every micro-batch of mb_seqs consecutive
+ * sequences (the last may be shorter) `logits_fn` is called on the calling
+ * thread to name that micro-batch's device logits — a trainer runs the model
+ * forward for those sequences there, on `stream` — and the fused loss pass
+ * runs on them; finally advantages and actor log-probs are copied back and the
+ * partials merged (merge_gradients).  Host array layout as
+ * rlo_objective_step_host.  The logits rows of micro-batch i are its own
+ * n_seqs*T padded rows (or packed via seq_start relative to the micro-batch).
+ * logits_fn fills *actor (required) and *old_logits / *ref_logits (leave
+ * data = NULL for "not given": old_logp / ref_logp host arrays are used).
+ * A non-RLO_OK return from logits_fn aborts the step with that status.
+ * Synchronises `stream`. */
+typedef rlo_status (*rlo_logits_fn)(void* user, int32_t micro_batch, int32_t seq_begin, int32_t n_seqs,
+                                    rlo_logits* actor, rlo_logits* old_logits, rlo_logits* ref_logits);
+rlo_status rlo_objective_step_host_mb(rlo_handle* h, const rlo_train_config* cfg, int32_t B, int32_t T,
+                                      int32_t mb_seqs, const int32_t* lengths, const int32_t* tokens,
+                                      const uint8_t* mask, const float* rewards_tok, const float* rewards_seq,
+                                      const float* values, rlo_logits_fn logits_fn, void* user,
+                                      const float* old_logp, const float* ref_logp, float* host_adv_out,
+                                      float* host_logp_out, rlo_stats* stats, void* stream);
 
 /* ---- next rows: the callers either side of the path ------ */
 

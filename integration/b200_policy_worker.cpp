@@ -87,6 +87,9 @@ void DeviceBatch::upload(const rollmini::SampleBatch& batch) {
       if (!s.advantages.empty()) adv[base + t] = static_cast<float>(s.advantages[t]);
       if (!s.rewards.empty()) rtok[base + t] = static_cast<float>(s.rewards[t]);
     }
+    // policy.cpp:266-271: a sample without per-token rewards scores its
+    // scalar_reward on the last response token
+    if (s.rewards.empty() && s.scalar_reward && n > 0) rtok[base + n - 1] = static_cast<float>(*s.scalar_reward);
     if (s.scalar_reward) rseq[static_cast<size_t>(b)] = static_cast<float>(*s.scalar_reward);
     has_mask_ |= !s.action_mask.empty();
     has_old_ |= !s.response_logprobs.empty();
@@ -138,6 +141,8 @@ std::vector<std::vector<double>> compute_advantages(rlo::Objective& obj, const r
         throw rollmini::InputError("compute_advantages: sample '" + s.sample_id + "' has no rewards");
     rlo::TrainConfig c = to_rlo(config);
     float* adv = db.scratch(0);
+    // per-token rewards (with scalar-only samples resolved onto their last
+    // token by upload) whenever any sample has them, else the scalar rewards
     obj.compute_advantages(c, db.view(), db.rewards(), db.rewards() ? nullptr : db.scalar_rewards(), nullptr, adv);
     obj.sync();
     return db.download(adv, batch);
@@ -146,8 +151,10 @@ std::vector<std::vector<double>> compute_advantages(rlo::Objective& obj, const r
 
 // ---- worker -------------------------------------------------------------------
 
-B200PolicyWorker::B200PolicyWorker(int32_t device, const rollmini::TrainConfig& train_config, LogitsProvider logits)
-    : obj_(device), train_config_(train_config), logits_(std::move(logits)), device_(device) {
+B200PolicyWorker::B200PolicyWorker(int32_t device, const rollmini::TrainConfig& train_config, LogitsProvider logits,
+                                   UpdateHook on_update)
+    : obj_(device), train_config_(train_config), logits_(std::move(logits)), on_update_(std::move(on_update)),
+      device_(device) {
   train_config_.validate();
   device_id = "cuda:" + std::to_string(device);
 }
@@ -159,6 +166,7 @@ rollmini::Message B200PolicyWorker::call(const std::string& method, const rollmi
   // policy_workers.cpp:46-64 dispatch for the path's methods
   if (method == "forward_logprobs") return do_forward_logprobs(input);
   if (method == "compute_gradient") return do_compute_gradient(input);
+  if (method == "apply_update") return do_apply_update(input);
   if (method == "get_version") {
     rollmini::Message out;
     out.fields["version"] = std::to_string(version_);
@@ -186,10 +194,16 @@ rollmini::Message B200PolicyWorker::do_forward_logprobs(const rollmini::Message&
 }
 
 rollmini::Message B200PolicyWorker::do_compute_gradient(const rollmini::Message& input) {
-  // policy_workers.cpp:111-121: per-rank GradAccum scalars; "dlogp" replaces
-  // the MLP parameter gradient (the model backward belongs to the trainer).
+  // policy_workers.cpp:111-121: the per-rank GradAccum scalars and tensors["grad"].
+  // The MLP parameter gradient of the reference has no counterpart here (the
+  // model backward belongs to the trainer), so "grad" is 0-dim -- which
+  // merge_gradients accepts (policy.cpp:421-430) and cluster_train_step
+  // forwards to apply_update as grad_mean -- and "dlogp" carries
+  // d(loss_t)/d(logp_t) per response token in sample order (policy.cpp:372-374).
   return translate([&] {
-    for (const auto& s : input.batch.samples) {  // policy.cpp:336-343, with the reference's sample ids
+    const rollmini::SampleBatch& batch = input.batch;
+    bool any_ref = false, any_noref = false;
+    for (const auto& s : batch.samples) {  // policy.cpp:336-343, with the reference's sample ids
       const size_t n = s.response_tokens.size();
       if (n == 0) continue;
       if (s.advantages.size() != n)
@@ -198,22 +212,65 @@ rollmini::Message B200PolicyWorker::do_compute_gradient(const rollmini::Message&
         throw rollmini::InputError("ppo_gradient: sample '" + s.sample_id + "' missing old logprobs");
       if (train_config_.kl_coef > 0.0 && s.ref_logprobs.size() != n)
         throw rollmini::InputError("ppo_gradient: sample '" + s.sample_id + "' missing ref logprobs");
+      (s.ref_logprobs.empty() ? any_noref : any_ref) = true;
     }
+    // kl_sum counts only samples that carry ref_logprobs (policy.cpp:368).
+    // With kl_coef == 0 a batch may mix both kinds: the samples with ref go
+    // first, as one view with ref log-probs, the others as a second view
+    // without (seq_offset keeps their records apart); dlogp is put back in
+    // sample order.
+    std::vector<size_t> order(batch.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+    size_t n_ref = batch.size();
+    if (any_ref && any_noref) {
+      std::stable_partition(order.begin(), order.end(),
+                            [&](size_t i) { return !batch.samples[i].ref_logprobs.empty(); });
+      n_ref = 0;
+      for (size_t i : order) n_ref += batch.samples[i].ref_logprobs.empty() ? 0 : 1;
+    } else if (!any_ref) {
+      n_ref = 0;
+    }
+    rollmini::SampleBatch perm;
+    for (size_t i : order) perm.push_back(batch.samples[i]);
     DeviceBatch db;
-    db.upload(input.batch);
-    const rlo_logits L = logits_(input.batch, db.T());
+    db.upload(perm);
+    const rlo_logits L = logits_(perm, db.T());
     rlo::TrainConfig c = to_rlo(train_config_);
-    rlo_token_out out_tok{};
-    out_tok.dlogp = db.scratch(1);
-    obj_.ppo_gradient(c, db.view(), L, nullptr, nullptr, db.old_logp(), db.ref_logp(),
-                      db.advantages() ? db.advantages() : db.scratch(2), &out_tok);
+    float* dlogp = db.scratch(1);
+    const float* adv = db.advantages() ? db.advantages() : db.scratch(2);
+    const int32_t T = db.T();
+    const rlo_batch all = db.view();
+    auto run = [&](int32_t b0, int32_t nb, bool with_ref) {
+      if (nb == 0) return;
+      const size_t off = static_cast<size_t>(b0) * static_cast<size_t>(T);
+      rlo_batch v = all;
+      v.B = nb;
+      v.seq_offset = b0;
+      v.lengths = all.lengths + b0;
+      v.tokens = all.tokens + off;
+      v.mask = all.mask ? all.mask + off : nullptr;
+      rlo_logits lv = L;
+      lv.data = static_cast<const char*>(L.data) +
+                off * static_cast<size_t>(L.row_stride) * (L.dtype == RLO_DTYPE_BF16 ? 2 : 4);
+      rlo_token_out out_tok{};
+      out_tok.dlogp = dlogp + off;
+      const float* old = db.old_logp();
+      const float* ref = with_ref ? db.ref_logp() : nullptr;
+      obj_.ppo_gradient(c, v, lv, nullptr, nullptr, old ? old + off : nullptr, ref ? ref + off : nullptr, adv + off,
+                        &out_tok);
+    };
+    run(0, static_cast<int32_t>(n_ref), true);
+    run(static_cast<int32_t>(n_ref), db.B() - static_cast<int32_t>(n_ref), false);
     // this rank's GradAccum scalars; zero tokens / non-finite values are the
     // controller's merge_gradients decision (policy.cpp:437-448)
     const rlo::Partials mine = obj_.rank_partials(c);
-    rollmini::Message out;
-    auto dl = db.download(out_tok.dlogp, input.batch);
+    auto dl = db.download(dlogp, perm);
+    std::vector<std::vector<double>> by_sample(batch.size());
+    for (size_t j = 0; j < order.size(); ++j) by_sample[order[j]] = std::move(dl[j]);
     std::vector<double> flat;
-    for (auto& v : dl) flat.insert(flat.end(), v.begin(), v.end());
+    for (auto& v : by_sample) flat.insert(flat.end(), v.begin(), v.end());
+    rollmini::Message out;
+    out.tensors["grad"] = {};
     out.tensors["dlogp"] = std::move(flat);
     out.scalars["loss_sum"] = mine.v[RLO_P_LOSS_SUM];
     out.scalars["ratio_sum"] = mine.v[RLO_P_RATIO_SUM];
@@ -224,9 +281,25 @@ rollmini::Message B200PolicyWorker::do_compute_gradient(const rollmini::Message&
   });
 }
 
-rollmini::WorkerFactory b200_worker_factory(const rollmini::TrainConfig& train_config, LogitsProvider logits) {
-  return [train_config, logits](int rank, int world_size, const std::string&) {
-    auto w = std::make_unique<B200PolicyWorker>(rank, train_config, logits);
+rollmini::Message B200PolicyWorker::do_apply_update(const rollmini::Message& input) {
+  // policy_workers.cpp:123-128 / policy.cpp:452-460: a zero learning rate is
+  // no update (the version stays); otherwise the trainer applies the step and
+  // the version advances.
+  const auto& grad_mean = input.tensor("grad_mean");
+  const double lr = input.scalar("learning_rate");
+  if (lr != 0.0) {
+    ++version_;
+    if (on_update_) on_update_(device_, lr, grad_mean, version_);
+  }
+  rollmini::Message out;
+  out.fields["version"] = std::to_string(version_);
+  return out;
+}
+
+rollmini::WorkerFactory b200_worker_factory(const rollmini::TrainConfig& train_config, LogitsProvider logits,
+                                            UpdateHook on_update) {
+  return [train_config, logits, on_update](int rank, int world_size, const std::string&) {
+    auto w = std::make_unique<B200PolicyWorker>(rank, train_config, logits, on_update);
     w->rank = rank;
     w->world_size = world_size;
     return w;

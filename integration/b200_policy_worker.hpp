@@ -27,6 +27,13 @@ namespace rollmini_b200 {
 // batch's b-th sample and t-th response position at data + (b*T + t)*row_stride.
 using LogitsProvider = std::function<rlo_logits(const rollmini::SampleBatch& batch, int32_t T)>;
 
+// apply_update (policy_workers.cpp:123-128, policy.cpp:452-460) on a B200
+// worker: the model parameters and their backward live in the trainer (the
+// path stops at dlogp / dlogits), so the worker hands the step to this hook:
+// (worker device, learning rate, merged grad_mean -- 0-dim here, new version).
+using UpdateHook = std::function<void(int32_t device, double learning_rate, const std::vector<double>& grad_mean,
+                                      uint64_t version)>;
+
 // Padded device copy of a SampleBatch (sample.hpp:16-60) for the C ABI.
 class DeviceBatch {
  public:
@@ -35,7 +42,10 @@ class DeviceBatch {
   DeviceBatch(const DeviceBatch&) = delete;
   DeviceBatch& operator=(const DeviceBatch&) = delete;
 
-  // T = longest response; per-token arrays that are empty in every sample are left null.
+  // T = longest response; per-token arrays that are empty in every sample are
+  // left null.  Rewards are resolved per sample as compute_advantages does
+  // (policy.cpp:265-276): per-token rewards, else scalar_reward on the last
+  // token -- so a batch mixing both kinds keeps every sample's reward.
   void upload(const rollmini::SampleBatch& batch);
   rlo_batch view() const;
   int32_t B() const { return B_; }
@@ -72,7 +82,8 @@ std::vector<std::vector<double>> compute_advantages(rlo::Objective& obj, const r
 
 class B200PolicyWorker : public rollmini::Worker {
  public:
-  B200PolicyWorker(int32_t device, const rollmini::TrainConfig& train_config, LogitsProvider logits);
+  B200PolicyWorker(int32_t device, const rollmini::TrainConfig& train_config, LogitsProvider logits,
+                   UpdateHook on_update = nullptr);
 
   rollmini::Message call(const std::string& method, const rollmini::Message& input) override;
 
@@ -81,15 +92,18 @@ class B200PolicyWorker : public rollmini::Worker {
  private:
   rollmini::Message do_forward_logprobs(const rollmini::Message& input);
   rollmini::Message do_compute_gradient(const rollmini::Message& input);
+  rollmini::Message do_apply_update(const rollmini::Message& input);
 
   rlo::Objective obj_;
   rollmini::TrainConfig train_config_;
   LogitsProvider logits_;
+  UpdateHook on_update_;
   uint64_t version_ = 1;
   int32_t device_ = 0;
 };
 
 // WorkerFactory (worker.hpp:47-48) for a cluster of B200 workers, one GPU each.
-rollmini::WorkerFactory b200_worker_factory(const rollmini::TrainConfig& train_config, LogitsProvider logits);
+rollmini::WorkerFactory b200_worker_factory(const rollmini::TrainConfig& train_config, LogitsProvider logits,
+                                            UpdateHook on_update = nullptr);
 
 }  // namespace rollmini_b200

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # RLO_LIB overrides the in-tree library (A/B builds of the same sources in kernel experiments).
 LIB_PATH = os.environ.get("RLO_LIB") or os.path.join(HERE, "lib", "librlo.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "rlo.h")
-ABI_VERSION = 4  # include/rlo.h RLO_ABI_VERSION: the struct layouts below
+ABI_VERSION = 5  # include/rlo.h RLO_ABI_VERSION: the struct layouts below
 
 RLO_OK, RLO_ERR_INPUT, RLO_ERR_CONFIG, RLO_ERR_TRAINING, RLO_ERR_CUDA, RLO_ERR_NCCL, RLO_ERR_DISPATCH = range(7)
 DTYPE_F32, DTYPE_BF16 = 0, 1
@@ -89,7 +89,14 @@ def declared_symbols() -> list[str]:
     with open(HEADER) as f:
         text = f.read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    text = re.sub(r"\btypedef\b[^;]*;", "", text)  # function-pointer types are not exports
     return sorted(set(re.findall(r"\b(rlo_[a-z0-9_]+)\s*\(", text)))
+
+
+# rlo_logits_fn (include/rlo.h): the per-micro-batch logits callback of
+# rlo_objective_step_host_mb.
+LOGITS_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(rlo_logits),
+                        C.POINTER(rlo_logits), C.POINTER(rlo_logits))
 
 
 def lib() -> C.CDLL:
@@ -130,6 +137,8 @@ def lib() -> C.CDLL:
                                 P(rlo_logits), vp, vp, vp, P(rlo_token_out), P(rlo_stats), vp], C.c_int),
         "rlo_objective_step_host": ([vp, P(rlo_train_config), i32, i32, vp, vp, vp, vp, vp, vp, P(rlo_logits),
                                      P(rlo_logits), P(rlo_logits), vp, vp, vp, vp, P(rlo_stats), vp], C.c_int),
+        "rlo_objective_step_host_mb": ([vp, P(rlo_train_config), i32, i32, i32, vp, vp, vp, vp, vp, vp,
+                                        LOGITS_FN, vp, vp, vp, vp, vp, P(rlo_stats), vp], C.c_int),
         "rlo_sync": ([vp, vp], C.c_int),
         "rlo_loss_weights": ([vp, P(rlo_train_config), P(rlo_batch), P(rlo_stats), vp, vp], C.c_int),
         "rlo_logits_backward": ([vp, P(rlo_batch), P(rlo_logits), vp, vp, vp, vp, i32, i64, vp], C.c_int),

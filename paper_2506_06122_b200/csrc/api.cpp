@@ -111,6 +111,11 @@ bool getenv_flag(const char* name) {
   return e && *e && *e != '0';
 }
 
+int getenv_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return (e && *e) ? std::atoi(e) : dflt;
+}
+
 struct DeviceGuard {
   int prev = -1, dev;
   explicit DeviceGuard(int d) : dev(d) {
@@ -149,9 +154,23 @@ struct DevBuf {
 
 }  // namespace
 
+Tuning rlo::read_tuning() {
+  Tuning t;
+  t.fused_off = getenv_flag("RLO_FUSED_OFF");
+  t.fused_slice_kb = getenv_int("RLO_FUSED_SLICE_KB", 0);
+  t.fused_nb = getenv_int("RLO_FUSED_NB", 2) == 3 ? 3 : 2;
+  t.fused_debug = getenv_flag("RLO_FUSED_DEBUG");
+  const char* me = std::getenv("RLO_DECODE_MARGIN");
+  t.decode_fixed_margin = me && *me;
+  t.decode_margin = t.decode_fixed_margin ? std::atof(me) : -1.0;
+  t.decode_noredo = getenv_flag("RLO_DECODE_NOREDO");
+  return t;
+}
+
 struct rlo_handle {
   int device = 0;
   int num_sms = 148;
+  Tuning tuning;  // environment knobs, read once here (internal.h)
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
   // accumulator of the loss pass (per sequence), reset by merge
@@ -304,7 +323,8 @@ rlo_status rlo_create(int32_t device, rlo_handle** out) {
   auto* h = new rlo_handle();
   h->device = device;
   h->num_sms = prop.multiProcessorCount;
-  if (h->err.ensure(1, true) != cudaSuccess || h->stats4.ensure(4, true) != cudaSuccess ||
+  h->tuning = read_tuning();
+  if (h->err.ensure(1) != cudaSuccess || cudaMemset(h->err.p, 0xFF, sizeof(DevError)) != cudaSuccess || h->stats4.ensure(4, true) != cudaSuccess ||
       h->partials.ensure(RLO_NPARTIAL, true) != cudaSuccess || h->stats_all.ensure(4, true) != cudaSuccess ||
       h->gathered.ensure(RLO_NPARTIAL, true) != cudaSuccess ||
       cudaMallocHost(&h->host_gathered, sizeof(double) * RLO_NPARTIAL) != cudaSuccess ||
@@ -325,6 +345,8 @@ rlo_status rlo_destroy(rlo_handle* h) {
   h->s_ratio.release();
   h->s_kl.release();
   h->s_ent.release();
+  h->s_dlogp.release();
+  h->s_lse64.release();
   h->s_flags.release();
   h->wstat.release();
   h->raw64.release();
@@ -402,15 +424,15 @@ rlo_status check_logits(const rlo_logits* l, const char* op, const char* which) 
   return RLO_OK;
 }
 
-rlo_status device_error_status(const DevError& e) {
-  if (e.code == DE_NONE) return RLO_OK;
-  switch (e.code) {
+rlo_status device_error_status(int32_t code, int32_t value) {
+  if (code == DE_NONE) return RLO_OK;
+  switch (code) {
     case DE_OOV_LOGPROB:  // policy.cpp:224-225
-      return fail(RLO_ERR_INPUT, "forward_logprobs: out-of-vocabulary token " + std::to_string(e.value));
+      return fail(RLO_ERR_INPUT, "forward_logprobs: out-of-vocabulary token " + std::to_string(value));
     case DE_OOV_LOSS:
-      return fail(RLO_ERR_INPUT, "ppo_gradient: out-of-vocabulary token " + std::to_string(e.value));
+      return fail(RLO_ERR_INPUT, "ppo_gradient: out-of-vocabulary token " + std::to_string(value));
     default:
-      return fail(RLO_ERR_INPUT, "sample batch: response length of sample '" + std::to_string(e.value) +
+      return fail(RLO_ERR_INPUT, "sample batch: response length of sample '" + std::to_string(value) +
                                      "' is outside [0, T]");
   }
 }
@@ -418,7 +440,9 @@ rlo_status device_error_status(const DevError& e) {
 rlo_status collect_device_error(rlo_handle* h, cudaStream_t s) {
   // h->host_err was filled by an async copy already synchronised by the caller
   (void)s;
-  return device_error_status(*h->host_err);
+  int32_t code = DE_NONE, value = 0;
+  dev_err_decode(h->host_err->key, &code, &value);
+  return device_error_status(code, value);
 }
 
 }  // namespace
@@ -428,7 +452,7 @@ rlo_status rlo_sync(rlo_handle* h, void* stream) {
   DeviceGuard g(h->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   RLO_CUDA(cudaMemcpyAsync(h->host_err, h->err.p, sizeof(DevError), cudaMemcpyDeviceToHost, s));
-  RLO_CUDA(cudaMemsetAsync(h->err.p, 0, sizeof(DevError), s));
+  RLO_CUDA(cudaMemsetAsync(h->err.p, 0xFF, sizeof(DevError), s));
   RLO_CUDA(cudaStreamSynchronize(s));
   return collect_device_error(h, s);
 }
@@ -452,6 +476,7 @@ rlo_status rlo_forward_logprobs(rlo_handle* h, const rlo_batch* batch, const rlo
   a.V = logits->V;
   a.B = batch->B;
   a.T = batch->T;
+  a.seq_offset = batch->seq_offset;
   a.lengths = batch->lengths;
   a.tokens = batch->tokens;
   a.mask = nullptr;  // forward_logprobs scores every response position (policy.cpp:223-229)
@@ -588,6 +613,7 @@ rlo_status ppo_setup(rlo_handle* h, const rlo_train_config* cfg, const rlo_batch
   a.V = actor->V;
   a.B = B;
   a.T = T;
+  a.seq_offset = batch->seq_offset;
   a.lengths = batch->lengths;
   a.tokens = batch->tokens;
   a.mask = batch->mask;
@@ -659,8 +685,8 @@ rlo_status rlo_ppo_gradient_fused(rlo_handle* h, const rlo_train_config* cfg, co
   if (empty) return RLO_OK;
   const int32_t B = batch->B, T = batch->T;
   int32_t slice = 0;
-  const int K = getenv_flag("RLO_FUSED_OFF") ? 0 : fused_cluster_size(a, grad, grad_dtype, grad_row_stride, &slice);
-  cudaError_t e = K > 0 ? launch_vocab_fused(a, weight, grad, grad_dtype, grad_row_stride, K, slice, s)
+  const int K = fused_cluster_size(a, grad, grad_dtype, grad_row_stride, h->tuning, &slice);
+  cudaError_t e = K > 0 ? launch_vocab_fused(a, weight, grad, grad_dtype, grad_row_stride, K, slice, h->tuning, s)
                         : cudaErrorNotSupported;
   if (e != cudaSuccess) {
     // not eligible (unaligned rows, vocab too large for a cluster's shared
@@ -703,7 +729,7 @@ rlo_status rlo_merge_gradients(rlo_handle* h, const rlo_train_config* cfg, rlo_s
     RLO_CUDA(cudaMemcpyAsync(h->host_gathered, h->partials.p, sizeof(double) * RLO_NPARTIAL, cudaMemcpyDeviceToHost, s));
   }
   RLO_CUDA(cudaMemcpyAsync(h->host_err, h->err.p, sizeof(DevError), cudaMemcpyDeviceToHost, s));
-  RLO_CUDA(cudaMemsetAsync(h->err.p, 0, sizeof(DevError), s));
+  RLO_CUDA(cudaMemsetAsync(h->err.p, 0xFF, sizeof(DevError), s));
   if (nseq > 0) RLO_CUDA(cudaMemsetAsync(h->recs.p, 0, sizeof(SeqRec) * static_cast<size_t>(nseq), s));
   h->acc_nseq = 0;
   RLO_CUDA(cudaStreamSynchronize(s));
@@ -749,8 +775,7 @@ rlo_status rlo_step_result_check(const rlo_step_result* r) {
     case 2: return fail(RLO_ERR_TRAINING, "training step aborted: non-finite gradient");
     case 3: return fail(RLO_ERR_TRAINING, "training step aborted: non-finite loss");
     default: {
-      DevError e{r->dev_error, r->dev_error_value};
-      return device_error_status(e);
+      return device_error_status(r->dev_error, r->dev_error_value);
     }
   }
 }
@@ -768,7 +793,7 @@ rlo_status rlo_rank_partials(rlo_handle* h, const rlo_train_config* cfg, rlo_par
   }
   RLO_CUDA(cudaMemcpyAsync(h->host_gathered, h->partials.p, sizeof(double) * RLO_NPARTIAL, cudaMemcpyDeviceToHost, s));
   RLO_CUDA(cudaMemcpyAsync(h->host_err, h->err.p, sizeof(DevError), cudaMemcpyDeviceToHost, s));
-  RLO_CUDA(cudaMemsetAsync(h->err.p, 0, sizeof(DevError), s));
+  RLO_CUDA(cudaMemsetAsync(h->err.p, 0xFF, sizeof(DevError), s));
   if (nseq > 0) RLO_CUDA(cudaMemsetAsync(h->recs.p, 0, sizeof(SeqRec) * static_cast<size_t>(nseq), s));
   h->acc_nseq = 0;
   RLO_CUDA(cudaStreamSynchronize(s));
@@ -834,6 +859,74 @@ rlo_status rlo_objective_step_host(rlo_handle* h, const rlo_train_config* cfg, i
                                  nullptr, stream));
   RLO_TRY(rlo_ppo_gradient(h, cfg, &batch, actor_logits, old_logits, ref_logits, old_logp ? h->h_old.p : nullptr,
                            ref_logp ? h->h_ref.p : nullptr, h->h_adv.p, &out, stream));
+  if (host_adv_out && N) RLO_CUDA(cudaMemcpyAsync(host_adv_out, h->h_adv.p, sizeof(float) * N, cudaMemcpyDeviceToHost, s));
+  if (host_logp_out && N)
+    RLO_CUDA(cudaMemcpyAsync(host_logp_out, h->h_logp.p, sizeof(float) * N, cudaMemcpyDeviceToHost, s));
+  return rlo_merge_gradients(h, cfg, stats, nullptr, stream);  // synchronises the stream
+}
+
+rlo_status rlo_objective_step_host_mb(rlo_handle* h, const rlo_train_config* cfg, int32_t B, int32_t T,
+                                      int32_t mb_seqs, const int32_t* lengths, const int32_t* tokens,
+                                      const uint8_t* mask, const float* rewards_tok, const float* rewards_seq,
+                                      const float* values, rlo_logits_fn logits_fn, void* user,
+                                      const float* old_logp, const float* ref_logp, float* host_adv_out,
+                                      float* host_logp_out, rlo_stats* stats, void* stream) {
+  if (!h) return fail(RLO_ERR_INPUT, "objective_step: null handle");
+  if (B < 0 || T < 0) return fail(RLO_ERR_INPUT, "objective_step: negative batch shape");
+  if ((int64_t)B * T > 0 && (!lengths || !tokens)) return fail(RLO_ERR_INPUT, "objective_step: lengths/tokens missing");
+  if (mb_seqs <= 0) return fail(RLO_ERR_CONFIG, "objective_step: micro-batch size must be positive");
+  if (!logits_fn) return fail(RLO_ERR_INPUT, "objective_step: logits callback required");
+  DeviceGuard g(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t N = static_cast<size_t>(B) * static_cast<size_t>(T);
+  const size_t nB = static_cast<size_t>(B);
+  auto up = [&](auto& buf, const auto* src, size_t n) -> cudaError_t {
+    using E = std::remove_pointer_t<decltype(buf.p)>;
+    if (!src || n == 0) return cudaSuccess;
+    cudaError_t e = buf.ensure(n);
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyAsync(buf.p, src, sizeof(E) * n, cudaMemcpyHostToDevice, s);
+  };
+  RLO_CUDA(up(h->h_lengths, lengths, nB));
+  RLO_CUDA(up(h->h_tokens, tokens, N));
+  RLO_CUDA(up(h->h_mask, mask, N));
+  RLO_CUDA(up(h->h_rtok, rewards_tok, N));
+  RLO_CUDA(up(h->h_rseq, rewards_seq, nB));
+  RLO_CUDA(up(h->h_values, values, N));
+  RLO_CUDA(up(h->h_old, old_logp, N));
+  RLO_CUDA(up(h->h_ref, ref_logp, N));
+  RLO_CUDA(h->h_adv.ensure(N));
+  RLO_CUDA(h->h_logp.ensure(N));
+  rlo_batch all{B, T, 0, 0, h->h_lengths.p, h->h_tokens.p, mask ? h->h_mask.p : nullptr};
+  RLO_TRY(rlo_compute_advantages(h, cfg, &all, rewards_tok ? h->h_rtok.p : nullptr,
+                                 rewards_seq ? h->h_rseq.p : nullptr, values ? h->h_values.p : nullptr, h->h_adv.p,
+                                 nullptr, stream));
+  // a failed micro-batch aborts the step: drop what the earlier ones accumulated
+  auto abort_step = [&](rlo_status st) {
+    if (h->acc_nseq > 0) cudaMemsetAsync(h->recs.p, 0, sizeof(SeqRec) * static_cast<size_t>(h->acc_nseq), s);
+    h->acc_nseq = 0;
+    cudaStreamSynchronize(s);
+    return st;
+  };
+  for (int32_t b0 = 0, i = 0; b0 < B; b0 += mb_seqs, ++i) {
+    const int32_t nb = std::min(mb_seqs, B - b0);
+    const size_t off = static_cast<size_t>(b0) * static_cast<size_t>(T);
+    rlo_logits la, lo, lr;
+    std::memset(&la, 0, sizeof(la));
+    std::memset(&lo, 0, sizeof(lo));
+    std::memset(&lr, 0, sizeof(lr));
+    const rlo_status cb = logits_fn(user, i, b0, nb, &la, &lo, &lr);
+    if (cb != RLO_OK)
+      return abort_step(fail(cb, "objective_step: logits callback failed for micro-batch " + std::to_string(i)));
+    rlo_batch mb{nb, T, b0, 0, h->h_lengths.p + b0, h->h_tokens.p + off, mask ? h->h_mask.p + off : nullptr};
+    rlo_token_out out;
+    std::memset(&out, 0, sizeof(out));
+    out.logp = host_logp_out ? h->h_logp.p + off : nullptr;
+    const rlo_status st = rlo_ppo_gradient(h, cfg, &mb, &la, lo.data ? &lo : nullptr, lr.data ? &lr : nullptr,
+                                           old_logp ? h->h_old.p + off : nullptr,
+                                           ref_logp ? h->h_ref.p + off : nullptr, h->h_adv.p + off, &out, stream);
+    if (st != RLO_OK) return abort_step(st);
+  }
   if (host_adv_out && N) RLO_CUDA(cudaMemcpyAsync(host_adv_out, h->h_adv.p, sizeof(float) * N, cudaMemcpyDeviceToHost, s));
   if (host_logp_out && N)
     RLO_CUDA(cudaMemcpyAsync(host_logp_out, h->h_logp.p, sizeof(float) * N, cudaMemcpyDeviceToHost, s));
@@ -972,7 +1065,8 @@ rlo_status rlo_decode_sample(rlo_handle* h, const rlo_logits* logits, int32_t n_
     return fail(RLO_ERR_INPUT, "decode: sample_keys, positions, out_tokens and out_logp are required");
   DeviceGuard g(h->device);
   RLO_CUDA(launch_decode(logits->data, logits->dtype, logits->row_stride, logits->V, n_rows, temperature, seed, version,
-                         sample_keys, positions, out_tokens, out_logp, h->num_sms, static_cast<cudaStream_t>(stream)));
+                         sample_keys, positions, out_tokens, out_logp, h->num_sms, h->tuning,
+                         static_cast<cudaStream_t>(stream)));
   return RLO_OK;
 }
 

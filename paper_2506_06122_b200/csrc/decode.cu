@@ -88,10 +88,9 @@ __device__ __forceinline__ float logit<__nv_bfloat16>(const __nv_bfloat16* p, in
 // ~20 of the library exp(); t < -708 is clamped (3e-308, below every sum it
 // enters).
 constexpr int kExpTab = 256;
-// Unclamped core: t must be >= -708 (the callers clamp the fp32 logit to
-// m - 700*T, one FMNMX, so -inf logits weigh exp(-700/T) ~ 1e-304 instead of 0
-// — below any sum they enter, as with the clamp).  2^k is added to the high
-// word only.
+// Unclamped core: t must be >= -708 (exp_neg clamps; -inf logits then weigh
+// exp(-708) ~ 3e-308 instead of 0 — below any sum they enter).  2^k is added
+// to the high word only.
 __device__ __forceinline__ double exp_neg_core(double t, const double* __restrict__ tab) {
   constexpr double kMagic = 6755399441055744.0;   // 1.5 * 2^52: round to integer
   constexpr double k256Ln2 = 369.32993046757462;  // 256 / ln 2
@@ -110,6 +109,16 @@ __device__ __forceinline__ double exp_neg_core(double t, const double* __restric
 }
 __device__ __forceinline__ double exp_neg(double t, const double* __restrict__ tab) {
   return exp_neg_core(fmax(t, -708.0), tab);  // branch-free: exp(-708) = 3e-308 stands in for 0
+}
+// The tempered exponent (x - M) / T of a logit x below the row max M, in fp64
+// (x - M is exact for fp32 / bf16 logits).  The clamp to exp_neg's domain is
+// applied AFTER the division by T: a bound formed in the logit domain
+// (M - 700*T in fp32) rounds to M itself at T <= 1e-9 and lets arguments below
+// -708 through at T ~ 1e-7 with |M| >= 128 (the reference decodes greedily at
+// T = 1e-6, pipeline.cpp:539).  -inf logits give -708 (3e-308), not NaN.
+__device__ __forceinline__ double scaled_gap(float x, double M, double inv_t, bool unit_t) {
+  const double d = (double)x - M;
+  return unit_t ? d : d * inv_t;
 }
 
 template <typename ET>
@@ -498,7 +507,6 @@ __global__ void __launch_bounds__(kDecWarps * 32)
   for (int j = threadIdx.x; j < kExpTab; j += blockDim.x) tab[j] = exp2((double)j / kExpTab);
   __syncthreads();
   const double inv_t = 1.0 / temp;
-  const float ftemp = (float)temp;
   const bool unit_t = temp == 1.0;
   const int W = ((V + kDecWarps - 1) / kDecWarps + 32 * E - 1) / (32 * E) * (32 * E);
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(logits) & 15u) == 0) && (((stride * (int64_t)sizeof(ET)) & 15) == 0);
@@ -507,7 +515,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
     const int v0 = warp * W, v1 = min(V, v0 + W);
     if (redo_only && out_tok[row] >= 0) continue;  // the screened kernel certified this row
     // pass 1
-    float m = -INFINITY, mL = kNegInit * kL2E, su = 0.f, lo = -INFINITY;
+    float m = -INFINITY, mL = kNegInit * kL2E, su = 0.f;
     double st = 0.0;
     for (int b = v0 + lane * E; b < v1; b += 32 * E) {
       float x[8];
@@ -518,7 +526,6 @@ __global__ void __launch_bounds__(kDecWarps * 32)
       if (cm > m) {
         if (m != -INFINITY) st *= exp_neg(unit_t ? (double)m - cm : ((double)m - cm) * inv_t, tab);
         m = cm;
-        lo = m - 700.f * ftemp;  // clamp bound for exp_neg_core
         const float nmL = __fmul_rn(cm, kL2E);
         su *= ex2(mL - nmL);
         mL = nmL;
@@ -528,8 +535,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
       float q[8];
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const double d = (double)fmaxf(x[e], lo) - (double)m;
-        w[e] = exp_neg_core(unit_t ? d : d * inv_t, tab);
+        w[e] = exp_neg(scaled_gap(x[e], (double)m, inv_t, unit_t), tab);
         q[e] = ex2(fmaf(x[e], kL2E, -mL));  // -inf -> ex2(-inf) = 0
       }
 #pragma unroll
@@ -594,7 +600,6 @@ __global__ void __launch_bounds__(kDecWarps * 32)
       // pass 2a: the 8 warps split the crossing warp's range into 8 sub-ranges
       // and sum their weights (relative to the row max) in parallel
       const double M = s_M;
-      const float loM = s_M - 700.f * ftemp;
       const int a0 = jw * W, a1 = min(V, a0 + W);
       const int W2 = ((W + kDecWarps - 1) / kDecWarps + 32 * E - 1) / (32 * E) * (32 * E);
       {
@@ -606,8 +611,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
           load_e<ET>(z, b, c1, vec_ok, x);
 #pragma unroll
           for (int e = 0; e < E; ++e) {
-            const double d = (double)fmaxf(x[e], loM) - M;
-            w[e] = b + e < c1 ? exp_neg_core(unit_t ? d : d * inv_t, tab) : 0.0;
+            w[e] = b + e < c1 ? exp_neg(scaled_gap(x[e], M, inv_t, unit_t), tab) : 0.0;
           }
 #pragma unroll
           for (int h = E / 2; h > 0; h >>= 1) {
@@ -649,8 +653,7 @@ __global__ void __launch_bounds__(kDecWarps * 32)
           load_e<ET>(z, b, c1, vec_ok, x);
 #pragma unroll
           for (int e = 0; e < E; ++e) {
-            const double d = (double)fmaxf(x[e], loM) - M;
-            w[e] = b + e < c1 ? exp_neg_core(unit_t ? d : d * inv_t, tab) : 0.0;
+            w[e] = b + e < c1 ? exp_neg(scaled_gap(x[e], M, inv_t, unit_t), tab) : 0.0;
             ls += w[e];
           }
           double incl = ls;
@@ -724,14 +727,13 @@ __global__ void __launch_bounds__(kDecWarps * 32, RLO_SCREEN_MINB)
 
 cudaError_t launch_decode(const void* logits, int32_t dtype, int64_t stride, int32_t V, int32_t n, double temperature,
                           uint64_t seed, uint64_t version, const uint64_t* keys, const uint64_t* positions,
-                          int32_t* out_tok, float* out_lp, int num_sms, cudaStream_t s) {
+                          int32_t* out_tok, float* out_lp, int num_sms, const Tuning& tu, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const int grid = n < num_sms * 8 ? n : num_sms * 8;
-  const char* me = std::getenv("RLO_DECODE_MARGIN");
-  // RLO_DECODE_MARGIN: a fixed margin instead of the derived one (<= 0: no screen)
-  const double fixed = (me && *me) ? std::atof(me) : -1.0;
+  // Tuning (read at rlo_create): a fixed margin instead of the derived one (<= 0: no screen)
+  const double fixed = tu.decode_fixed_margin ? tu.decode_margin : -1.0;
   const double eps_e = screen_eps(V);
-  const bool screen = !(me && *me) || fixed > 0.0;
+  const bool screen = !tu.decode_fixed_margin || fixed > 0.0;
   const bool bf = dtype == RLO_DTYPE_BF16;
   if (screen) {
     if (bf)
@@ -745,8 +747,7 @@ cudaError_t launch_decode(const void* logits, int32_t dtype, int64_t stride, int
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
   const bool redo = screen;  // the fp64 kernel redoes only the rows the screen left (out_tok = -1)
-  const char* nr = std::getenv("RLO_DECODE_NOREDO");  // diagnostics: leave the screen's -1 marks (fail rate)
-  if (redo && nr && *nr == '1') return cudaGetLastError();
+  if (redo && tu.decode_noredo) return cudaGetLastError();  // diagnostics: leave the screen's -1 marks
   if (bf)
     decode_kernel<__nv_bfloat16><<<grid, kDecWarps * 32, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(logits), stride,
                                                                   V, n, temperature, seed, version, keys,

@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
         }
       }
       if (lane == 0) {
-        if (oov && r == 0) flag_error(a, DE_OOV_LOSS, tok);
+        if (oov && r == 0) flag_error(a, DE_OOV_LOSS, global_row(a, row), tok);
         const double nan = __longlong_as_double(0x7ff8000000000000LL);
         double lp[NT];
 #pragma unroll
@@ -375,13 +375,8 @@ __global__ void __launch_bounds__(kFTotal, 3) fused_kernel(const FusedArgs f) {
   cl.sync();  // DSMEM lifetime: no CTA exits while a peer may still read its slots
 }
 
-int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return (e && *e) ? std::atoi(e) : dflt;
-}
-
 template <typename ET, typename GT, int NT, int NB>
-cudaError_t launch_t(const FusedArgs& f, int K, cudaStream_t s) {
+cudaError_t launch_t(const FusedArgs& f, int K, bool debug, cudaStream_t s) {
   constexpr int U = sizeof(ET) == 4 ? 8 : 4;
   constexpr int MATH = sizeof(ET) == 4 ? 1 : 6;  // the vocab pass's measured defaults
   auto kern = fused_kernel<ET, GT, NT, U, MATH, NB>;
@@ -407,7 +402,7 @@ cudaError_t launch_t(const FusedArgs& f, int K, cudaStream_t s) {
   const int64_t nrows = (int64_t)f.v.B * f.v.T;
   if (ncl > nrows) ncl = (int)nrows;
   cfg.gridDim = dim3((unsigned)(ncl * K));
-  if (env_int("RLO_FUSED_DEBUG", 0))
+  if (debug)
     fprintf(stderr, "[rlo] fused pass: K=%d slice=%d smem=%zu clusters=%d\n", K, f.slice, smem, ncl);
   e = cudaLaunchKernelEx(&cfg, kern, f);
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -415,11 +410,11 @@ cudaError_t launch_t(const FusedArgs& f, int K, cudaStream_t s) {
 }
 
 template <typename ET, typename GT, int NB>
-cudaError_t launch_nb(const FusedArgs& f, int K, cudaStream_t s) {
+cudaError_t launch_nb(const FusedArgs& f, int K, bool debug, cudaStream_t s) {
   switch (f.v.ntens) {
-    case 1: return launch_t<ET, GT, 1, NB>(f, K, s);
-    case 2: return launch_t<ET, GT, 2, NB>(f, K, s);
-    default: return launch_t<ET, GT, 3, NB>(f, K, s);
+    case 1: return launch_t<ET, GT, 1, NB>(f, K, debug, s);
+    case 2: return launch_t<ET, GT, 2, NB>(f, K, debug, s);
+    default: return launch_t<ET, GT, 3, NB>(f, K, debug, s);
   }
 }
 
@@ -427,8 +422,8 @@ cudaError_t launch_nb(const FusedArgs& f, int K, cudaStream_t s) {
 // actor slices in flight), giving the epilogue and the cluster another row of
 // slack at the cost of shared memory (A/B knob, profiles/r1_fused.txt).
 template <typename ET, typename GT>
-cudaError_t launch_nt(const FusedArgs& f, int K, cudaStream_t s) {
-  return env_int("RLO_FUSED_NB", 2) == 3 ? launch_nb<ET, GT, 3>(f, K, s) : launch_nb<ET, GT, 2>(f, K, s);
+cudaError_t launch_nt(const FusedArgs& f, int K, const Tuning& tu, cudaStream_t s) {
+  return tu.fused_nb == 3 ? launch_nb<ET, GT, 3>(f, K, tu.fused_debug, s) : launch_nb<ET, GT, 2>(f, K, tu.fused_debug, s);
 }
 
 }  // namespace
@@ -443,14 +438,16 @@ cudaError_t launch_nt(const FusedArgs& f, int K, cudaStream_t s) {
 // 8.3 ms) — the bf16 pass is bound by SM power, not bytes — so bf16 stays
 // two-pass.  RLO_FUSED_SLICE_KB overrides the budget (and then allows any
 // dtype and clusters up to 8) for experiments.
-int fused_cluster_size(const VocabArgs& a, const void* grad, int32_t gdtype, int64_t gstride, int32_t* slice) {
+int fused_cluster_size(const VocabArgs& a, const void* grad, int32_t gdtype, int64_t gstride, const Tuning& tu,
+                       int32_t* slice) {
+  if (tu.fused_off) return 0;
   const int esz = a.dtype == RLO_DTYPE_BF16 ? 2 : 4, gsz = gdtype == RLO_DTYPE_BF16 ? 2 : 4;
   const int E = 16 / esz;
   for (int k = 0; k < a.ntens; ++k)
     if ((reinterpret_cast<uintptr_t>(a.logits[k]) & 15u) || ((a.stride[k] * esz) & 15)) return 0;
   const int gal = E * gsz < 16 ? E * gsz : 16;  // widest gradient store
   if ((reinterpret_cast<uintptr_t>(grad) % gal) || ((gstride * gsz) % gal)) return 0;
-  const int forced = vocab::env_int("RLO_FUSED_SLICE_KB", 0);
+  const int forced = tu.fused_slice_kb;
   if (forced <= 0 && a.dtype == RLO_DTYPE_BF16) return 0;  // measured slower than two passes for bf16 (see above)
   const int64_t budget = (int64_t)(forced > 0 ? forced : 32) * 1024;
   const int kmax = forced > 0 ? 8 : 4;
@@ -466,7 +463,7 @@ int fused_cluster_size(const VocabArgs& a, const void* grad, int32_t gdtype, int
 }
 
 cudaError_t launch_vocab_fused(const VocabArgs& a, const float* weight, void* grad, int32_t gdtype, int64_t gstride,
-                               int K, int32_t slice, cudaStream_t s) {
+                               int K, int32_t slice, const Tuning& tu, cudaStream_t s) {
   using namespace vocab;
   if ((int64_t)a.B * a.T == 0) return cudaSuccess;
   FusedArgs f;
@@ -476,9 +473,9 @@ cudaError_t launch_vocab_fused(const VocabArgs& a, const float* weight, void* gr
   f.gstride = gstride;
   f.slice = slice;
   if (a.dtype == RLO_DTYPE_BF16)
-    return gdtype == RLO_DTYPE_BF16 ? launch_nt<__nv_bfloat16, __nv_bfloat16>(f, K, s)
-                                    : launch_nt<__nv_bfloat16, float>(f, K, s);
-  return gdtype == RLO_DTYPE_BF16 ? launch_nt<float, __nv_bfloat16>(f, K, s) : launch_nt<float, float>(f, K, s);
+    return gdtype == RLO_DTYPE_BF16 ? launch_nt<__nv_bfloat16, __nv_bfloat16>(f, K, tu, s)
+                                    : launch_nt<__nv_bfloat16, float>(f, K, tu, s);
+  return gdtype == RLO_DTYPE_BF16 ? launch_nt<float, __nv_bfloat16>(f, K, tu, s) : launch_nt<float, float>(f, K, tu, s);
 }
 
 }  // namespace rlo

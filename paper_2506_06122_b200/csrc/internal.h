@@ -11,6 +11,13 @@
 
 #include "../../include/rlo.h"
 
+#if defined(__CUDACC__)
+#define RLO_HOST_DEVICE __host__ __device__
+#else
+#define RLO_HOST_DEVICE
+#endif
+
+
 namespace rlo {
 
 extern std::atomic<uint64_t> g_launches;
@@ -24,12 +31,36 @@ enum Role : int32_t { ROLE_ACTOR = 0, ROLE_OLD = 1, ROLE_REF = 2 };
 // Per-token flag bits written by the loss epilogue.
 enum : uint8_t { TF_CLIPPED = 1, TF_DUAL = 2, TF_NONFINITE_GRAD = 4, TF_NONFINITE_LOSS = 8 };
 
-// Device error slot: first failure wins (atomicCAS on code).
+// Device error slot.  The reference raises the FIRST failure in sample order
+// (policy.cpp:223-225 walks samples, then positions), so the slot keeps the
+// minimum of a 64-bit key over every failing row (atomicMin; no ordering
+// between CTAs needed):  key = class:2 | position:30 | value:32, with class
+// 0 = response length outside [0, T] (position = sequence, value = sequence),
+// 1 = OOV token in forward_logprobs, 2 = OOV token in the loss pass
+// (position = global row (seq_offset + b) * T + t, value = the token id).
+// A length error therefore wins over any OOV token, and the earliest row wins
+// among OOV tokens.  kDevErrNone (all ones) = no error; reset by memset 0xFF.
 enum : int32_t { DE_NONE = 0, DE_OOV_LOGPROB = 1, DE_OOV_LOSS = 2, DE_BAD_LENGTH = 3 };
+constexpr unsigned long long kDevErrNone = ~0ull;
 struct DevError {
-  int32_t code;
-  int32_t value;  // offending token id or sequence index
+  unsigned long long key;
 };
+RLO_HOST_DEVICE inline unsigned long long dev_err_key(int32_t code, int64_t pos, int32_t value) {
+  const unsigned long long cls = code == DE_BAD_LENGTH ? 0ull : code == DE_OOV_LOGPROB ? 1ull : 2ull;
+  const unsigned long long p = pos < 0 ? 0ull : pos > 0x3FFFFFFF ? 0x3FFFFFFFull : (unsigned long long)pos;
+  return (cls << 62) | (p << 32) | (unsigned long long)(uint32_t)value;
+}
+// Decoded slot: code DE_* (DE_NONE when empty) and its value.
+RLO_HOST_DEVICE inline void dev_err_decode(unsigned long long key, int32_t* code, int32_t* value) {
+  if (key == kDevErrNone) {
+    *code = DE_NONE;
+    *value = 0;
+    return;
+  }
+  const unsigned long long cls = key >> 62;
+  *code = cls == 0 ? DE_BAD_LENGTH : cls == 1 ? DE_OOV_LOGPROB : DE_OOV_LOSS;
+  *value = (int32_t)(uint32_t)(key & 0xFFFFFFFFull);
+}
 
 // Per-sequence record of the loss pass (fp64 sums in a fixed order).
 struct SeqRec {
@@ -43,11 +74,6 @@ struct WStat {
   double sum, sq, count, pad;
 };
 
-#if defined(__CUDACC__)
-#define RLO_HOST_DEVICE __host__ __device__
-#else
-#define RLO_HOST_DEVICE
-#endif
 
 // Whitening parameters from rank-ordered statistics stats_all[r*4 + {0,1,2}] =
 // (sum, sum of squares, count) over masked positions (policy.cpp:288-302):
@@ -102,6 +128,28 @@ RLO_HOST_DEVICE inline int32_t merge_stats(const double* parts, int32_t world, i
   return isfinite(o.loss) ? 0 : 3;
 }
 
+// Diagnostic / experiment knobs, read ONCE from the environment when a
+// handle is created (rlo_create) and never per launch.  None of them changes
+// the numerics of the default path beyond its stated tolerance: they select
+// the fused pass's slice budget and pipeline depth (or switch it off), and
+// the decode screen's certificate margin.
+//   RLO_FUSED_OFF=1          fused update pass -> two-pass form
+//   RLO_FUSED_SLICE_KB=n     per-CTA actor slice budget (also enables bf16 rows)
+//   RLO_FUSED_NB=3           three actor slices in flight instead of two
+//   RLO_FUSED_DEBUG=1        print the fused launch shape
+//   RLO_DECODE_MARGIN=x      fixed certificate margin (<= 0: fp64 path only)
+//   RLO_DECODE_NOREDO=1      leave the screen's -1 marks (measures its fail rate)
+struct Tuning {
+  bool fused_off = false;
+  int fused_slice_kb = 0;
+  int fused_nb = 2;
+  bool fused_debug = false;
+  bool decode_fixed_margin = false;
+  double decode_margin = -1.0;
+  bool decode_noredo = false;
+};
+Tuning read_tuning();
+
 struct VocabArgs {
   const void* logits[3];
   int64_t stride[3];
@@ -111,6 +159,7 @@ struct VocabArgs {
   int32_t dtype;  // rlo_dtype shared by all tensors of the pass
   int32_t V;
   int32_t B, T;
+  int32_t seq_offset;  // first sequence of this view in the rank-local batch (error ordering)
   const int32_t* lengths;
   const int32_t* tokens;
   const uint8_t* mask;
@@ -165,9 +214,10 @@ cudaError_t launch_vocab_logprob(const VocabArgs& a, int num_sms, cudaStream_t s
 cudaError_t launch_vocab_loss(const VocabArgs& a, int num_sms, cudaStream_t s);
 // Fused update pass (fused.cu): cluster size K (0 = not eligible) and the
 // per-CTA slice length, then the launch.
-int fused_cluster_size(const VocabArgs& a, const void* grad, int32_t gdtype, int64_t gstride, int32_t* slice);
+int fused_cluster_size(const VocabArgs& a, const void* grad, int32_t gdtype, int64_t gstride, const Tuning& tu,
+                       int32_t* slice);
 cudaError_t launch_vocab_fused(const VocabArgs& a, const float* weight, void* grad, int32_t gdtype, int64_t gstride,
-                               int K, int32_t slice, cudaStream_t s);
+                               int K, int32_t slice, const Tuning& tu, cudaStream_t s);
 cudaError_t launch_seq_reduce(int32_t B, int32_t T, int32_t seq_offset, const int32_t* lengths,
                               const uint8_t* mask, const float* s_loss, const float* s_ratio,
                               const float* s_kl, const float* s_ent, const uint8_t* s_flags, SeqRec* recs,
@@ -197,7 +247,7 @@ cudaError_t launch_value_loss(int32_t B, int32_t T, const int32_t* lengths, cons
                               double* seqsums, double* out4, cudaStream_t s);
 cudaError_t launch_decode(const void* logits, int32_t dtype, int64_t stride, int32_t V, int32_t n, double temperature,
                           uint64_t seed, uint64_t version, const uint64_t* keys, const uint64_t* positions,
-                          int32_t* out_tok, float* out_lp, int num_sms, cudaStream_t s);
+                          int32_t* out_tok, float* out_lp, int num_sms, const Tuning& tu, cudaStream_t s);
 cudaError_t launch_synth_logits(void* dst, int32_t dtype, int64_t rows, int32_t V, int64_t row_stride,
                                 uint64_t seed, int32_t model_id, int64_t row_key_offset, cudaStream_t s);
 cudaError_t launch_synth_tokens(int32_t* dst, int64_t rows, int32_t V, uint64_t seed, int64_t row_key_offset,

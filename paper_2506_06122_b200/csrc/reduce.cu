@@ -122,13 +122,11 @@ __global__ void merge_finalize_kernel(const double* __restrict__ parts, int worl
                                       rlo_step_result* out) {
   rlo_step_result r;
   r.stats = rlo_stats{};
-  r.dev_error = err->code;
-  r.dev_error_value = err->value;
+  dev_err_decode(err->key, &r.dev_error, &r.dev_error_value);
   r.reason = r.dev_error ? 4 : merge_stats(parts, world, agg, &r.stats);
   r.status = r.reason == 0 ? RLO_OK : r.reason == 4 ? RLO_ERR_INPUT : RLO_ERR_TRAINING;
   *out = r;
-  err->code = 0;
-  err->value = 0;
+  err->key = kDevErrNone;
 }
 
 }  // namespace

@@ -151,7 +151,16 @@ __device__ __forceinline__ void pair2(float zl, float zh, f2 L2, f2 nmL, f2& s, 
   const f2 t = ffma2(pk2(zl, zh), L2, nmL);
   float tl, th;
   upk2(t, tl, th);
-  if ((ENT && GUARD) || poly) {  // poly: clamp to the polynomial's normal-range domain
+  if (poly) {
+    // the polynomial's domain: 2^j is inserted into the exponent field, so j
+    // must stay in [-126, 127].  The upper clamp matters under the lazy max
+    // and lockstep streams, where t can be positive: an element far above the
+    // running max then yields 2^127 (the chunk sum fails the lazy cap / the
+    // lockstep range check and is redone the exact way) instead of a wrapped
+    // exponent that would silently drop the dominant term.
+    tl = fminf(fmaxf(tl, -126.0f), 127.0f);
+    th = fminf(fmaxf(th, -126.0f), 127.0f);
+  } else if (ENT && GUARD) {
     tl = fmaxf(tl, -126.0f);
     th = fmaxf(th, -126.0f);
   }
@@ -382,8 +391,12 @@ __device__ __forceinline__ RowResult finish(const Acc& a) {
   return r;
 }
 
-__device__ __forceinline__ void flag_error(const VocabArgs& a, int code, int value) {
-  if (atomicCAS(&a.err->code, 0, code) == 0) a.err->value = value;
+// Row of token (b, t) in the rank-local batch across micro-batches: (seq_offset + b) * T + t.
+__device__ __forceinline__ int64_t global_row(const VocabArgs& a, int64_t row) { return row + (int64_t)a.seq_offset * a.T; }
+
+// Report a failing row; the slot keeps the earliest in sample order (internal.h).
+__device__ __forceinline__ void flag_error(const VocabArgs& a, int code, int64_t pos, int value) {
+  atomicMin(&a.err->key, dev_err_key(code, pos, value));
 }
 
 // Loss epilogue for one loss-participating token (policy.cpp:355-374 + extensions), fp64.
@@ -482,7 +495,7 @@ __device__ __forceinline__ bool row_active(const VocabArgs& a, int64_t row, bool
   const int t = (int)(row - (int64_t)b * a.T);
   if (report && t == 0) {
     const int raw = __ldg(a.lengths + b);
-    if (raw < 0 || raw > a.T) flag_error(a, DE_BAD_LENGTH, b);
+    if (raw < 0 || raw > a.T) flag_error(a, DE_BAD_LENGTH, (int64_t)a.seq_offset + b, a.seq_offset + b);
   }
   bool active = t < seq_len(a.lengths, b, a.T);
   if (LOSS && active && a.mask) active = __ldg(a.mask + row) != 0;
@@ -553,7 +566,7 @@ __device__ __forceinline__ void row_finish_acc(const VocabArgs& a, Acc (&c)[NT],
     if (k == 0) ent = r.entropy;
   }
   if (lane != 0) return;
-  if (oov) flag_error(a, LOSS ? DE_OOV_LOSS : DE_OOV_LOGPROB, tok);
+  if (oov) flag_error(a, LOSS ? DE_OOV_LOSS : DE_OOV_LOGPROB, global_row(a, row), tok);
   const double nan = __longlong_as_double(0x7ff8000000000000LL);
   double lp[NT];
 #pragma unroll

@@ -479,6 +479,50 @@ class Objective:
         return UpdateStats.from_c(st)
 
 
+    def step_host_mb(self, cfg: TrainConfig, tokens: np.ndarray, lengths: np.ndarray, mb_seqs: int, logits_fn,
+                     mask=None, rewards=None, scalar_rewards=None, values=None, old_logprobs=None,
+                     ref_logprobs=None, adv_out=None, logp_out=None, stream=None) -> UpdateStats:
+        """Micro-batched reference-facing step (rlo_objective_step_host_mb):
+        host SampleBatch arrays for the whole batch, advantages over the whole
+        batch, then ``logits_fn(i, seq_begin, n_seqs)`` -> (actor, old, ref)
+        device tensors (old/ref may be None) names each micro-batch's logits
+        (called on this thread, in order, before that micro-batch's pass)."""
+        B, T = tokens.shape
+        st = _abi.rlo_stats()
+        keep = []
+        err = []
+
+        def hp(a):
+            if a is None:
+                return None
+            if hasattr(a, "data_ptr"):
+                return C.c_void_p(a.data_ptr())
+            return a.ctypes.data_as(C.c_void_p)
+
+        def cb(_user, i, b0, nb, pa, po, pr):
+            try:
+                ts = logits_fn(int(i), int(b0), int(nb))
+                for t, dst in zip(ts, (pa, po, pr)):
+                    if t is not None:
+                        L = _logits(t)
+                        keep.append(t)
+                        dst[0] = L
+                return 0
+            except Exception as e:  # surfaced after the call returns
+                err.append(e)
+                return _abi.RLO_ERR_INPUT
+
+        fn = _abi.LOGITS_FN(cb)
+        rc = _abi.lib().rlo_objective_step_host_mb(
+            self._h, C.byref(cfg.to_c()), B, T, mb_seqs, hp(lengths), hp(tokens), hp(mask), hp(rewards),
+            hp(scalar_rewards), hp(values), fn, None, hp(old_logprobs), hp(ref_logprobs), hp(adv_out), hp(logp_out),
+            C.byref(st), _stream(stream, self.device))
+        if err:
+            raise err[0]
+        check(rc)
+        return UpdateStats.from_c(st)
+
+
 def synth_logits(dst, seed: int, model: int, row_key_offset: int = 0, stream=None) -> None:
     """Fill a [rows, V] (row-strided) float32/bfloat16 CUDA tensor with the
     deterministic synthetic logits of include/rlo_synth.h."""

@@ -235,6 +235,96 @@ int main() {
           "reference Cluster + cluster_forward_logprobs over 2 B200 workers == reference forward_logprobs");
   }
 
+  // 6) compute_advantages on a batch MIXING per-token and scalar-only rewards
+  //    (policy.cpp:265-276 resolves the source per sample)
+  {
+    SampleBatch mixed = batch;
+    for (size_t i = 1; i < mixed.size(); i += 2) {
+      auto& r = mixed.samples[i];
+      r.rewards.clear();
+      r.scalar_reward = 0.25 + 0.5 * static_cast<double>(i);
+    }
+    TrainConfig c2 = cfg;
+    c2.gamma = 0.9;
+    for (bool whiten : {false, true}) {
+      c2.whiten_advantages = whiten;
+      const auto ra = compute_advantages(mixed, c2);
+      const auto ga = rollmini_b200::compute_advantages(b200.objective(), mixed, c2);
+      double worst = 0.0;
+      for (size_t i = 0; i < ra.size(); ++i)
+        for (size_t t = 0; t < ra[i].size(); ++t)
+          worst = std::max(worst, std::fabs(ga[i][t] - ra[i][t]) / std::max(1.0, std::fabs(ra[i][t])));
+      check(worst <= 2e-5, std::string("mixed per-token / scalar rewards: compute_advantages matches (whiten ") +
+                               (whiten ? "on" : "off") + ", max scaled err " + std::to_string(worst) + ")");
+    }
+  }
+
+  // 7) compute_gradient with kl_coef = 0 on a batch where some samples carry
+  //    no ref_logprobs: kl_sum counts only the samples that do (policy.cpp:368)
+  {
+    TrainConfig c0 = cfg;
+    c0.kl_coef = 0.0;
+    PolicyWorker ref0(params, Vocabulary::standard(), c0);
+    rollmini_b200::B200PolicyWorker b0(0, c0, provider);
+    Message mix = in;
+    mix.batch.samples[1].ref_logprobs.clear();
+    mix.batch.samples[4].ref_logprobs.clear();
+    Message a = ref0.call("compute_gradient", mix);
+    Message b = b0.call("compute_gradient", mix);
+    bool ok = true;
+    for (const char* k : {"loss_sum", "ratio_sum", "kl_sum"}) ok &= close(b.scalar(k), a.scalar(k));
+    ok &= b.scalar("clipped") == a.scalar("clipped") && b.scalar("tokens") == a.scalar("tokens");
+    size_t ntok = 0;
+    for (const auto& r : mix.batch.samples) ntok += r.response_tokens.size();
+    ok &= b.tensor("dlogp").size() == ntok;
+    check(ok, "mixed ref_logprobs presence (kl_coef 0): scalars match (kl_sum " + std::to_string(b.scalar("kl_sum")) +
+                  " vs " + std::to_string(a.scalar("kl_sum")) + ")");
+    // dlogp is returned in sample order: equal to a batch without the
+    // permutation when every sample carries ref (kl_coef 0: ref does not enter dlogp)
+    Message full = b0.call("compute_gradient", in);
+    check(full.tensor("dlogp") == b.tensor("dlogp"), "mixed-ref dlogp is returned in sample order");
+  }
+
+  // 8) the reference's own training controller, cluster_train_step
+  //    (policy_workers.cpp:208-232: compute_gradient over shards ->
+  //    merge_gradients -> apply_update broadcast), unchanged, over 2 B200
+  //    workers vs over 2 reference PolicyWorkers
+  {
+    int ndev = 0;
+    cudaGetDeviceCount(&ndev);
+    std::vector<BindingAssignment> assign = {{0, "g0"}, {1, "g1"}};
+    std::mutex mu;
+    std::vector<std::pair<int, double>> updates;
+    size_t grad_dim = 99;
+    rollmini_b200::UpdateHook hook = [&](int32_t device, double lr, const std::vector<double>& g, uint64_t ver) {
+      std::lock_guard<std::mutex> lock(mu);
+      updates.emplace_back(device, lr);
+      grad_dim = g.size();
+      (void)ver;
+    };
+    auto bfac = [&provider, &cfg, &hook, ndev](int rank, int world, const std::string&) -> std::unique_ptr<Worker> {
+      auto w = std::make_unique<rollmini_b200::B200PolicyWorker>(rank % std::max(ndev, 1), cfg, provider, hook);
+      w->rank = rank;
+      w->world_size = world;
+      return w;
+    };
+    Cluster b200_train(Role::actor_train, 2, assign, bfac);
+    Cluster ref_train(Role::actor_train, 2, assign, policy_worker_factory(params, Vocabulary::standard(), cfg));
+    const UpdateStats sb = cluster_train_step(b200_train, batch, cfg);
+    const UpdateStats sa = cluster_train_step(ref_train, batch, cfg);
+    check(close(sb.loss, sa.loss) && close(sb.mean_ratio, sa.mean_ratio) && close(sb.mean_kl, sa.mean_kl) &&
+              close(sb.clip_fraction, sa.clip_fraction) && sb.tokens == sa.tokens,
+          "cluster_train_step over 2 B200 workers == over 2 reference PolicyWorkers (loss " +
+              std::to_string(sb.loss) + " vs " + std::to_string(sa.loss) + ", tokens " + std::to_string(sb.tokens) +
+              ")");
+    const Message v0 = b200_train.call_rank(0, "get_version", {});
+    const Message r0 = ref_train.call_rank(0, "get_version", {});
+    check(updates.size() == 2 && grad_dim == 0 && updates[0].second == cfg.learning_rate &&
+              v0.field("version") == r0.field("version"),
+          "apply_update reached every B200 rank (lr " + std::to_string(cfg.learning_rate) + "), version " +
+              v0.field("version") + " == reference " + r0.field("version"));
+  }
+
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "OK", g_fail);
   return g_fail ? 1 : 0;
 }

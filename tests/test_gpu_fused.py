@@ -113,10 +113,11 @@ def test_fused_matches_two_pass_and_oracle(env, dt, gdt, V, P, agg):
 def test_fused_kernel_forced_for_bf16_qwen_vocab(env, monkeypatch):
     """The bf16 Qwen row runs two-pass by default (measured faster); force the
     8-CTA cluster kernel and check it against the same oracle."""
-    monkeypatch.setenv("RLO_FUSED_SLICE_KB", "40")
-    test_fused_matches_two_pass_and_oracle(env, "bf16", "bf16", 152064, 3, 1)
+    torch, rlo, _ = env
+    monkeypatch.setenv("RLO_FUSED_SLICE_KB", "40")  # knobs are read when a handle is created
+    test_fused_matches_two_pass_and_oracle((torch, rlo, rlo.Objective(0)), "bf16", "bf16", 152064, 3, 1)
     monkeypatch.setenv("RLO_FUSED_SLICE_KB", "16")  # 8 CTAs x 19 KB, fp32 with a bf16 gradient
-    test_fused_matches_two_pass_and_oracle(env, "f32", "bf16", 32000, 2, 3)
+    test_fused_matches_two_pass_and_oracle((torch, rlo, rlo.Objective(0)), "f32", "bf16", 32000, 2, 3)
 
 
 def test_fused_micro_batches_and_neg_inf(env):
@@ -199,6 +200,8 @@ def test_fused_errors(env):
 
 def test_fused_three_slices_in_flight(env, monkeypatch):
     """RLO_FUSED_NB=3 (gradient written two rows late) gives the same results."""
-    monkeypatch.setenv("RLO_FUSED_NB", "3")
-    test_fused_matches_two_pass_and_oracle(env, "f32", "f32", 32000, 3, 1)
-    test_fused_matches_two_pass_and_oracle(env, "f32", "bf16", 4099, 1, 3)
+    torch, rlo, _ = env
+    monkeypatch.setenv("RLO_FUSED_NB", "3")  # read when the handle is created
+    obj = rlo.Objective(0)
+    test_fused_matches_two_pass_and_oracle((torch, rlo, obj), "f32", "f32", 32000, 3, 1)
+    test_fused_matches_two_pass_and_oracle((torch, rlo, obj), "f32", "bf16", 4099, 1, 3)

@@ -247,7 +247,8 @@ def test_decode_sample_cdf_boundary_draws(env, dt, temp, monkeypatch):
     toks = {}
     for mg in ("", "0", "1"):
         monkeypatch.setenv("RLO_DECODE_MARGIN", mg)
-        t, lp = obj.decode_sample(x, temp, seed, ver, kd, pd)
+        o = rlo.Objective(0)  # the margin knob is read when a handle is created
+        t, lp = o.decode_sample(x, temp, seed, ver, kd, pd)
         toks[mg] = t.cpu().numpy()
         lp = lp.cpu().numpy()
         for j in range(n):

@@ -251,48 +251,6 @@ def test_fused_loss_vs_oracle(env, dtype, agg, kl_est):
     assert abs(st.dual_clip_fraction - want["dual_clip_fraction"]) * st.tokens <= 1
 
 
-@pytest.mark.parametrize("impl,math,ldg", [
-    ("tma", None, None), ("ldg", "0", None), ("tma", "0", None),                # fp32 mixes and producers
-    ("ldg", "1", None), ("ldg", "2", None), ("ldg", "3", None), ("ldg", "4", None), ("ldg", "5", None),
-    ("tma", "4", None), ("ldg", None, "1"), ("ldg", None, "2"), ("ldg", None, "3"),  # bf16 mixes / layouts
-    ("ldg", None, "4"), ("ldg", "4", "4"),                                         # bf16 lockstep streams
-    ("epi", None, None), ("epi", "0", None),                                       # epilogue-warp kernel
-])
-def test_vocab_variants_vs_oracle(env, monkeypatch, impl, math, ldg):
-    """Every selectable producer (LDG / TMA ring), instruction mix (RLO_VOCAB_MATH)
-    and LDG layout (RLO_VOCAB_LDG) against the oracle, both dtypes, with -inf
-    entries in the actor rows (the guarded entropy redo)."""
-    monkeypatch.setenv("RLO_VOCAB_IMPL", "ldg" if impl == "epi" else impl)
-    if impl == "epi":
-        monkeypatch.setenv("RLO_VOCAB_EPI", "1")
-    if math is not None:
-        monkeypatch.setenv("RLO_VOCAB_MATH", math)
-    if ldg is not None:
-        monkeypatch.setenv("RLO_VOCAB_LDG", ldg)
-    for dtype in (O.F32, O.BF16):
-        if dtype == O.F32 and math not in (None, "0", "1"):
-            continue
-        if dtype == O.BF16 and math == "0":
-            continue
-        torch, rlo, obj = env
-        rng = np.random.default_rng(77)
-        B, T, V = 6, 9, 4096 if dtype == O.F32 else 16384  # several load batches per row on every path
-        lengths, tokens, mask, adv, rows = _random_case(rng, B, T, V, dtype)
-        ninf, half = (-np.inf, 0.5) if dtype == O.F32 else (0xFF80, 0x3F00)  # bf16 bit patterns
-        rows[0][3, ::7] = ninf
-        rows[0][3, tokens.ravel()[3]] = half
-        cfg = rlo.TrainConfig(kl_coef=0.05, kl_estimator="k3")
-        outs = obj.ppo_gradient(cfg, dev(torch, tokens), dev(torch, lengths), _dev_logits(torch, rows[0], dtype),
-                                dev(torch, adv), mask=dev(torch, mask), old_logits=_dev_logits(torch, rows[1], dtype),
-                                ref_logits=_dev_logits(torch, rows[2], dtype), outputs=("logp", "old_logp", "entropy"))
-        obj.merge_gradients(cfg)
-        lps = [O.forward_logprobs(r, dtype, V, V, B, T, lengths, tokens) for r in rows]
-        m = (mask.ravel() != 0) & (np.arange(T)[None, :] < lengths[:, None]).ravel()
-        assert_close(outs["logp"].cpu().numpy().ravel()[m], lps[0][0][m], what=f"logp {impl} {math} {ldg}")
-        assert_close(outs["old_logp"].cpu().numpy().ravel()[m], lps[1][0][m], what="old_logp")
-        assert_close(outs["entropy"].cpu().numpy().ravel()[m], lps[0][1][m], what="entropy")
-
-
 def test_actor_only_with_precomputed_old_ref(env):
     torch, rlo, obj = env
     rng = np.random.default_rng(9)
@@ -462,8 +420,9 @@ def test_full_size_config2_properties(env):
     cfg1 = rlo.TrainConfig()
     obj.ppo_gradient(cfg1, toks, lengths, L[0], adv, old_logits=L[0])
     st1 = obj.merge_gradients(cfg1)
-    # exactly 1 when both rows use the same exp2 path; within 1e-7 when RLO_VOCAB_MATH>=2 sends part of
-    # the old-policy row's exponentials through the FMA-pipe polynomial (relative error 1.9e-7 per term)
+    # exactly 1 when both rows use the same exp2 path; within 1e-7 when the bf16 mix sends part of
+    # the old-policy row's exponentials through the FMA-pipe polynomial (relative error <= 2.9e-6 per
+    # term, on a quarter of the pairs)
     assert abs(st1.mean_ratio - 1.0) <= 1e-7 and close(st1.loss, -float(adv.double().mean()), 1e-6)
     del L
     torch.cuda.empty_cache()
