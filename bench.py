@@ -479,7 +479,7 @@ def oracle_check(O, c, seed, check):
         want = z[int(tok)] - lse
         worst = max(worst, abs(float(g) - want) / max(1.0, abs(want)))
     return {"rows": len(rows), "what": "actor logp of sampled rows of the last timed step vs oracle",
-            "max_scaled_err": worst, "tol": 1e-5, "ok": worst <= 1e-5}
+            "max_scaled_err": float(worst), "tol": 1e-5, "ok": bool(worst <= 1e-5)}
 
 
 def cpu_baseline(args, c, target_s=12.0, use_ref=None, check=None):

@@ -119,8 +119,10 @@ __device__ __forceinline__ void acc_warp_reduce(Acc& a) {
 // MATH -> polynomial degree of the offloaded pairs (0: none) and whether half
 // (rather than a quarter) of the old/ref element pairs are offloaded.
 __host__ __device__ constexpr int poly_deg(int math) {
-  return math == 2 || math == 3 ? 5 : math == 4 || math == 5 || math == 6 ? 4 : 0;
+  return math == 2 || math == 3 ? 5 : math == 4 || math == 5 || math == 6 || math == 9 ? 4 : 0;
 }
+// mix 9: as 6 with the polynomial on the .y word of every other vector only (12.5%).
+__host__ __device__ constexpr bool poly_odd_only(int math) { return math == 9; }
 __host__ __device__ constexpr bool poly_half(int math) { return math == 3 || math == 5; }
 __host__ __device__ constexpr int poly_deg_ent(int math) { return math == 4 ? 4 : 0; }
 // Template MATH values may carry kMathGuard (the guarded entropy-row variant).
@@ -235,13 +237,18 @@ struct Vec<float> {
       const f2 L2 = pk2(kL2E, kL2E), nmL = pk2(-mL, -mL);
       f2 s0 = 0, s1 = 0, w0 = 0, w1 = 0;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        pair2<ENT, G>(v[u].x, v[u].y, L2, nmL, s0, w0, 0);
-        pair2<ENT, G>(v[u].z, v[u].w, L2, nmL, s1, w1, (!ENT && (u & 1)) ? poly_deg(MATH) : 0);
-      }
+      for (int u = 0; u < U; ++u) vec_sums<ENT, MATHG>(v[u], u, L2, nmL, s0, s1, w0, w1);
       cs = hsum2(s0, s1);
       if (ENT) cw = hsum2(w0, w1);
     }
+  }
+  // One vector (position u of its batch) into packed accumulators (MATH != 0).
+  template <bool ENT, int MATHG>
+  __device__ static void vec_sums(const V& v, int u, f2 L2, f2 nmL, f2& s0, f2& s1, f2& w0, f2& w1) {
+    constexpr int MATH = MATHG & kMathMask;
+    constexpr bool G = (MATHG & kMathGuard) != 0;
+    pair2<ENT, G>(v.x, v.y, L2, nmL, s0, w0, 0);
+    pair2<ENT, G>(v.z, v.w, L2, nmL, s1, w1, (!ENT && (u & 1)) ? poly_deg(MATH) : 0);
   }
   template <int U, bool ENT, int MATHG>
   __device__ static void accumulate(const V (&v)[U], Acc& a) {
@@ -288,15 +295,22 @@ struct Vec<__nv_bfloat16> {
       const f2 L2 = pk2(kL2E, kL2E), nmL = pk2(-mL, -mL);
       f2 s0 = 0, s1 = 0, w0 = 0, w1 = 0;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        pair2<ENT, G>(bf16lo(v[u].x), bf16hi(v[u].x), L2, nmL, s0, w0, 0);
-        pair2<ENT, G>(bf16lo(v[u].y), bf16hi(v[u].y), L2, nmL, s1, w1, ENT ? poly_deg_ent(MATH) : poly_deg(MATH));
-        pair2<ENT, G>(bf16lo(v[u].z), bf16hi(v[u].z), L2, nmL, s0, w0, 0);
-        pair2<ENT, G>(bf16lo(v[u].w), bf16hi(v[u].w), L2, nmL, s1, w1, (ENT || !poly_half(MATH)) ? 0 : poly_deg(MATH));
-      }
+      for (int u = 0; u < U; ++u) vec_sums<ENT, MATHG>(v[u], u, L2, nmL, s0, s1, w0, w1);
       cs = hsum2(s0, s1);
       if (ENT) cw = hsum2(w0, w1);
     }
+  }
+  // One vector into packed accumulators (MATH != 0): the polynomial lanes are
+  // the .y word (and, for half offload, the .w word) of every vector.
+  template <bool ENT, int MATHG>
+  __device__ static void vec_sums(const V& v, int u, f2 L2, f2 nmL, f2& s0, f2& s1, f2& w0, f2& w1) {
+    constexpr int MATH = MATHG & kMathMask;
+    constexpr bool G = (MATHG & kMathGuard) != 0;
+    const int py = ENT ? poly_deg_ent(MATH) : (poly_odd_only(MATH) && !(u & 1)) ? 0 : poly_deg(MATH);
+    pair2<ENT, G>(bf16lo(v.x), bf16hi(v.x), L2, nmL, s0, w0, 0);
+    pair2<ENT, G>(bf16lo(v.y), bf16hi(v.y), L2, nmL, s1, w1, py);
+    pair2<ENT, G>(bf16lo(v.z), bf16hi(v.z), L2, nmL, s0, w0, 0);
+    pair2<ENT, G>(bf16lo(v.w), bf16hi(v.w), L2, nmL, s1, w1, (ENT || !poly_half(MATH)) ? 0 : poly_deg(MATH));
   }
   template <int U, bool ENT, int MATHG>
   __device__ static void accumulate(const V (&v)[U], Acc& a) {

@@ -280,9 +280,23 @@ int main() {
     check(ok, "mixed ref_logprobs presence (kl_coef 0): scalars match (kl_sum " + std::to_string(b.scalar("kl_sum")) +
                   " vs " + std::to_string(a.scalar("kl_sum")) + ")");
     // dlogp is returned in sample order: equal to a batch without the
-    // permutation when every sample carries ref (kl_coef 0: ref does not enter dlogp)
+    // permutation when every sample carries ref (kl_coef 0: ref does not enter
+    // dlogp) -- up to fp32 rounding, since permuting the samples moves these
+    // 148-byte rows to other 16-byte alignments (another summation split)
     Message full = b0.call("compute_gradient", in);
-    check(full.tensor("dlogp") == b.tensor("dlogp"), "mixed-ref dlogp is returned in sample order");
+    const auto& dm = b.tensor("dlogp");
+    const auto& df = full.tensor("dlogp");
+    size_t first_bad = dm.size() == df.size() ? dm.size() : 0;
+    for (size_t i = 0; i < std::min(dm.size(), df.size()); ++i)
+      if (!close(dm[i], df[i], 1e-6)) {
+        first_bad = i;
+        break;
+      }
+    check(first_bad == dm.size(), "mixed-ref dlogp is returned in sample order" +
+                                      (first_bad < dm.size() ? " (first difference at " + std::to_string(first_bad) +
+                                                                   ": " + std::to_string(dm[first_bad]) + " vs " +
+                                                                   std::to_string(df[first_bad]) + ")"
+                                                             : std::string()));
   }
 
   // 8) the reference's own training controller, cluster_train_step
