@@ -160,6 +160,10 @@ def run_ours(args, c):
     dist = None
     if world > 1:
         import torch.distributed as dist
+        # NCCL's communicator-init lines (rank, nranks, NVLink/NVLS topology) go to
+        # stderr with the run, so a scaling record can confirm the group it ran on
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     obj = rlo.Objective(local)
     if world > 1:
