@@ -28,6 +28,13 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+
+if int(os.environ.get("WORLD_SIZE", "1")) > 1 and os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+    # NCCL's communicator-init lines (rank, nranks, NVLink / NVLS topology) go to
+    # stderr with an N > 1 run, so a scaling record can confirm the group it ran
+    # on; set before torch loads NCCL, which reads the level once
+    os.environ["NCCL_DEBUG"] = "INFO"
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 sys.path.insert(0, ROOT)
 
 METRIC = "scored tokens/sec (logprob+KL+adv+PPO loss); HBM GB/s vs peak; 1/2/4/8 GPU"
@@ -160,10 +167,6 @@ def run_ours(args, c):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        # NCCL's communicator-init lines (rank, nranks, NVLink/NVLS topology) go to
-        # stderr with the run, so a scaling record can confirm the group it ran on
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     obj = rlo.Objective(local)
     if world > 1:
@@ -438,25 +441,29 @@ def run_e2e(args, c, obj, rlo, torch, cfg, logits, side, dev, stream, dist, key_
             "d2h_bytes_per_step": hb_out + 64, "api": api, "ms_per_step": 1e3 * el / args.steps}
 
 
-def kernel_source_hash():
-    """sha256 over the CUDA sources of the library (csrc/*.cu, *.cuh, *.h):
-    identifies the kernels a stored ncu capture was taken from."""
-    import glob
+def kernel_sass_hash(lib=None):
+    """sha256 of the SASS of every kernel in the library this run loaded
+    (cuobjdump -sass, addresses stripped): identifies the kernels a stored ncu
+    capture was taken from, independent of host-code or comment changes."""
     import hashlib
-    h = hashlib.sha256()
-    src = os.path.join(ROOT, "paper_2506_06122_b200", "csrc")
-    for p in sorted(glob.glob(os.path.join(src, "*.cu")) + glob.glob(os.path.join(src, "*.cuh")) +
-                    glob.glob(os.path.join(src, "*.h"))):
-        with open(p, "rb") as f:
-            h.update(os.path.basename(p).encode() + b"\0" + f.read())
-    return h.hexdigest()[:16]
+    import re
+    import subprocess
+    from paper_2506_06122_b200 import _abi
+    lib = lib or _abi.LIB_PATH
+    try:
+        out = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True, timeout=120).stdout
+    except Exception:
+        return None
+    body = "\n".join(re.sub(r"/\*[0-9a-f]{4,}\*/|/\* 0x[0-9a-f]+ \*/", "", ln).strip()
+                     for ln in out.splitlines() if "Function :" in ln or re.match(r"\s+/\*[0-9a-f]{4,}\*/", ln))
+    return hashlib.sha256(body.encode()).hexdigest()[:16]
 
 
 def traffic_from_profile(cfg_id):
     """DRAM bytes per launch of the vocab kernel from the committed ncu
     capture (profiles/ncu_traffic.json, written by tools/ncu_traffic.py) --
-    used only when that capture was taken from the kernel sources this run
-    was built from (source hash match); otherwise null, never a stale value."""
+    used only when that capture was taken from the very kernels this run
+    loaded (SASS hash match); otherwise null, never a stale value."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None, "no capture"
@@ -465,9 +472,9 @@ def traffic_from_profile(cfg_id):
     v = d.get(f"cfg{cfg_id}")
     if v is None:
         return None, "no capture for this config"
-    if v.get("src_hash") != kernel_source_hash():
-        return None, "capture is from other kernel sources (stale): not used"
-    return v.get("bytes_per_launch"), f"ncu capture {v.get('capture', '')} (src {v.get('src_hash')})"
+    if v.get("sass_hash") != kernel_sass_hash():
+        return None, "capture is from other kernels (SASS hash differs: stale): not used"
+    return v.get("bytes_per_launch"), f"ncu capture {v.get('capture', '')} (kernel SASS {v.get('sass_hash')})"
 
 
 def oracle_check(O, c, seed, check):
