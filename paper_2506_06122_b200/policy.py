@@ -550,35 +550,68 @@ class Message:
 
 class PolicyWorker:
     """Worker plugin for the path's methods (policy_workers.cpp:46-64):
-    ``forward_logprobs`` fills ``batch['ref_logprobs']`` (:93-100) and
-    ``compute_gradient`` returns the GradAccum scalars (:111-121).  The
-    batch carries the model's logits under ``batch['logits']``."""
+    ``forward_logprobs`` fills ``batch['ref_logprobs']`` (:93-100);
+    ``compute_gradient`` returns the GradAccum scalars and ``tensors['grad']``
+    (:111-121) -- 0-dim here, the model backward belongs to the trainer --
+    plus ``tensors['dlogp']``; ``apply_update`` (:123-128, policy.cpp:452-460)
+    advances the version (a zero learning rate is no update) and hands the
+    step to ``on_update(learning_rate, grad_mean, version)``; ``get_version``.
+    The batch carries the model's logits under ``batch['logits']``."""
 
-    METHODS = ("forward_logprobs", "compute_gradient")
+    METHODS = ("forward_logprobs", "compute_gradient", "apply_update", "get_version")
 
-    def __init__(self, device: int, train_config: TrainConfig, rank: int = 0, world_size: int = 1):
+    def __init__(self, device: int, train_config: TrainConfig, rank: int = 0, world_size: int = 1,
+                 on_update=None):
         train_config.validate()
         self.rank, self.world_size, self.device_id = rank, world_size, f"cuda:{device}"
         self.train_config = train_config
         self.obj = Objective(device)
+        self.version = 1
+        self.on_update = on_update
 
     def call(self, method: str, msg: Message) -> Message:
         if method == "forward_logprobs":
             b = msg.batch
             lp = self.obj.forward_logprobs(b["logits"], b["response_tokens"], b["lengths"])["logp"]
-            out = Message(batch=dict(b), fields={"version": msg.fields.get("version", "0")})
+            out = Message(batch=dict(b), fields={"version": str(self.version)})
             out.batch["ref_logprobs"] = lp
             return out
         if method == "compute_gradient":
             b = msg.batch
-            self.obj.ppo_gradient(self.train_config, b["response_tokens"], b["lengths"], b["logits"],
-                                  b["advantages"], mask=b.get("action_mask"), old_logprobs=b["response_logprobs"],
-                                  ref_logprobs=b.get("ref_logprobs"), outputs=("dlogp",))
+            res = self.obj.ppo_gradient(self.train_config, b["response_tokens"], b["lengths"], b["logits"],
+                                        b["advantages"], mask=b.get("action_mask"),
+                                        old_logprobs=b["response_logprobs"], ref_logprobs=b.get("ref_logprobs"),
+                                        outputs=("dlogp",))
             p = self.obj.rank_partials(self.train_config)
             out = Message()
+            out.tensors = {"grad": [], "dlogp": res["dlogp"]}
             out.scalars = {"loss_sum": p[0], "ratio_sum": p[1], "kl_sum": p[2], "clipped": p[4], "tokens": p[6]}
             return out
+        if method == "apply_update":
+            lr = float(msg.scalars["learning_rate"])
+            grad_mean = msg.tensors.get("grad_mean", [])
+            if lr != 0.0:
+                self.version += 1
+                if self.on_update is not None:
+                    self.on_update(lr, grad_mean, self.version)
+            return Message(fields={"version": str(self.version)})
+        if method == "get_version":
+            return Message(fields={"version": str(self.version)})
         raise DispatchError(f"policy worker: unimplemented method '{method}'")
+
+
+def cluster_train_step(workers, shards, config: TrainConfig) -> UpdateStats:
+    """cluster_train_step (policy_workers.cpp:208-232) over in-process workers:
+    compute_gradient on each rank's shard, merge_gradients of the rank-ordered
+    GradAccum scalars (policy.cpp:421-450), apply_update broadcast."""
+    replies = [w.call("compute_gradient", Message(batch=s)) for w, s in zip(workers, shards)]
+    parts = np.zeros((len(replies), _abi.NPARTIAL))
+    for r, rep in enumerate(replies):
+        parts[r, [0, 1, 2, 4, 6]] = [rep.scalars[k] for k in ("loss_sum", "ratio_sum", "kl_sum", "clipped", "tokens")]
+    stats = merge_partials(parts, config)
+    for w in workers:
+        w.call("apply_update", Message(tensors={"grad_mean": []}, scalars={"learning_rate": config.learning_rate}))
+    return stats
 
 
 def sample_key(sample_id: str) -> int:

@@ -366,8 +366,24 @@ def test_policy_worker_plugin(env):
               "response_logprobs": old, "advantages": dev(torch, adv)}
     rep = w.call("compute_gradient", rlo.Message(batch=batch2))
     assert rep.scalars["tokens"] == int(lengths.sum())
+    assert len(rep.tensors["grad"]) == 0 and rep.tensors["dlogp"].shape == (B, T)
     with pytest.raises(rlo.DispatchError):
         w.call("generate", rlo.Message())
+    # the reference controller's step over two workers (policy_workers.cpp:208-232):
+    # rank-ordered merge of the shards == one worker over the whole batch, then
+    # apply_update advances every worker's version (policy.cpp:452-460)
+    seen = []
+    ws = [rlo.PolicyWorker(0, rlo.TrainConfig(), rank=r, world_size=2,
+                           on_update=lambda lr, g, v: seen.append((lr, len(g), v))) for r in range(2)]
+    half = lambda d, s: {k: v[s] for k, v in d.items() if k != "logits"} | {  # noqa: E731
+        "logits": d["logits"].view(B, T, V)[s].reshape(-1, V)}
+    st2 = rlo.cluster_train_step(ws, [half(batch2, slice(0, 2)), half(batch2, slice(2, 4))], rlo.TrainConfig())
+    st1 = rlo.merge_partials(np.array([[rep.scalars.get(k, 0.0) for k in ("loss_sum", "ratio_sum", "kl_sum")] +
+                                       [0.0, rep.scalars["clipped"], 0.0, rep.scalars["tokens"]] + [0.0] * 9]),
+                             rlo.TrainConfig())
+    assert close(st2.loss, st1.loss, 1e-12) and st2.tokens == st1.tokens
+    assert seen == [(0.05, 0, 2), (0.05, 0, 2)]
+    assert all(w.call("get_version", rlo.Message()).fields["version"] == "2" for w in ws)
 
 
 def test_full_size_config2_properties(env):

@@ -52,7 +52,8 @@ def bench_decode(obj):
         for temp in (0.8, 1.0):
             for margin in ("", "0"):  # screened fp32 path (default) / fp64 path only
                 os.environ["RLO_DECODE_MARGIN"] = margin
-                ms = timed(lambda: obj.decode_sample(x, temp, 42, 3, keys, pos))
+                o = rlo.Objective(obj.device)  # knobs are read when a handle is created
+                ms = timed(lambda: o.decode_sample(x, temp, 42, 3, keys, pos))
                 print(json.dumps({"row": "decode", "rows": rows, "V": V, "stride": stride,
                                   "dtype": str(dt).split(".")[-1], "temperature": temp,
                                   "path": "fp64" if margin == "0" else "screened", "ms": ms,

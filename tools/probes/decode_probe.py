@@ -18,14 +18,15 @@ for _ in range(3):
     tok, lp = obj.decode_sample(x, temp, 42, 3, keys, pos)
 torch.cuda.synchronize()
 os.environ["RLO_DECODE_MARGIN"] = "0"
-tok64, _ = obj.decode_sample(x, temp, 42, 3, keys, pos)
+tok64, _ = rlo.Objective(0).decode_sample(x, temp, 42, 3, keys, pos)  # knobs: read at handle creation
 print("tokens screened == fp64:", bool((tok == tok64).all().item()), "rows", rows)
 # rows the screen leaves to the fp64 kernel
 os.environ.pop("RLO_DECODE_MARGIN")
 if os.environ.get("MARGIN"):
     os.environ["RLO_DECODE_MARGIN"] = os.environ["MARGIN"]
 os.environ["RLO_DECODE_NOREDO"] = "1"
+probe = rlo.Objective(0)
 for t in (0.6, 0.8, 1.0, 1.3):
-    tk, _ = obj.decode_sample(x, t, 42, 3, keys, pos)
+    tk, _ = probe.decode_sample(x, t, 42, 3, keys, pos)
     print(f"V={V} T={t} margin={os.environ.get('MARGIN', 'default')}: screen fail rate {(tk < 0).float().mean().item():.3f}")
 os.environ.pop("RLO_DECODE_NOREDO")
