@@ -1,0 +1,145 @@
+// power_probe.cu — where the bf16 vocab pass's energy goes under the 1 kW cap.
+// Streams three tensors of R rows x 304128 bytes (Qwen-vocabulary bf16 rows)
+// with the vocab kernel's layout (persistent #SM x 4 CTAs x 256 threads, U=4
+// 16-byte ld.global.nc.L1::no_allocate per thread per batch) for a fixed wall
+// time, with one of several amounts of work per element:
+//   0 xor     : one LOP3 per 32-bit word (the memory system alone)
+//   1 fma     : bf16 unpack + FFMA2 (t = z*log2e - m) + FADD2 (sum of t): the
+//               FMA-pipe part of the real pass without the exponential
+//   2 mufu    : 1 + MUFU.EX2 per element (sum of 2^t): the real pass's math
+//               without the online max / lazy check / polynomial lanes
+//   3 mufu+w  : 2 + the entropy FFMA2 on every element
+// The wrapper (tools/probes/power_probe.sh) samples SM clock and board power
+// with nvidia-smi while each mode runs.  Build:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/power_probe tools/probes/power_probe.cu
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+using f2 = unsigned long long;
+__device__ __forceinline__ f2 pk2(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ f2 ffma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2 fadd2(f2 a, f2 b) {
+  f2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int MODE>
+__device__ __forceinline__ void word(uint32_t x, f2 L2, f2 nm, f2& s, f2& w, uint32_t& acc) {
+  if (MODE == 0) {
+    acc ^= x;
+    return;
+  }
+  const f2 t = ffma2(pk2(__uint_as_float(x << 16), __uint_as_float(x & 0xFFFF0000u)), L2, nm);
+  if (MODE == 1) {
+    s = fadd2(s, t);
+    return;
+  }
+  float tl, th;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(tl), "=f"(th) : "l"(t));
+  const f2 e = pk2(ex2(tl), ex2(th));
+  s = fadd2(s, e);
+  if (MODE == 3) w = ffma2(e, t, w);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 4) probe_kernel(const uint4* t0, const uint4* t1, const uint4* t2, int64_t rows,
+                                                       int nvec, float* out) {
+  __shared__ float red[8];
+  const uint4* ts[3] = {t0, t1, t2};
+  const int tid = threadIdx.x;
+  const f2 L2 = pk2(1.4426950408889634f, 1.4426950408889634f), nm = pk2(-3.0f, -3.0f);
+  f2 s = 0, w = 0;
+  uint32_t acc = 0;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+#pragma unroll 1
+    for (int k = 0; k < 3; ++k) {
+      const uint4* row = ts[k] + r * nvec + tid;
+      for (int base = 0; base + 1024 <= nvec; base += 1024) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = ld_stream(row + base + u * 256);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          word<MODE>(v[u].x, L2, nm, s, w, acc);
+          word<MODE>(v[u].y, L2, nm, s, w, acc);
+          word<MODE>(v[u].z, L2, nm, s, w, acc);
+          word<MODE>(v[u].w, L2, nm, s, w, acc);
+        }
+      }
+    }
+    float sl, sh;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(sl), "=f"(sh) : "l"(fadd2(s, w)));
+    if ((tid & 31) == 0) red[tid >> 5] = sl + sh + (float)acc;
+    __syncthreads();
+  }
+  if (tid == 0 && red[0] == 1234.5f) out[0] = red[1];  // keep the work
+}
+
+int main(int argc, char** argv) {
+  const int mode = argc > 1 ? atoi(argv[1]) : 0;
+  const double secs = argc > 2 ? atof(argv[2]) : 6.0;
+  const int64_t rows = 32768, rb = 304128;
+  const int nvec = (int)(rb / 16);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  uint4* t[3];
+  for (int k = 0; k < 3; ++k) {
+    cudaMalloc(&t[k], rows * rb);
+    cudaMemset(t[k], 0x3F + k, rows * rb);  // bf16 words ~0.5..1.5: finite exponentials
+  }
+  float* out;
+  cudaMalloc(&out, 4);
+  auto launch = [&]() {
+    switch (mode) {
+      case 0: probe_kernel<0><<<sms * 4, 256>>>(t[0], t[1], t[2], rows, nvec, out); break;
+      case 1: probe_kernel<1><<<sms * 4, 256>>>(t[0], t[1], t[2], rows, nvec, out); break;
+      case 2: probe_kernel<2><<<sms * 4, 256>>>(t[0], t[1], t[2], rows, nvec, out); break;
+      default: probe_kernel<3><<<sms * 4, 256>>>(t[0], t[1], t[2], rows, nvec, out); break;
+    }
+  };
+  for (int i = 0; i < 3; ++i) launch();
+  cudaDeviceSynchronize();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const auto w0 = std::chrono::steady_clock::now();
+  int n = 0;
+  cudaEventRecord(e0);
+  while (std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count() < secs) {
+    for (int i = 0; i < 20; ++i) launch();
+    n += 20;
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+  }
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double bytes = 3.0 * rows * (double)(nvec / 1024 * 1024) * 16 * n;
+  printf("power_probe mode=%d: %d launches, %.3f ms/launch, %.0f GB/s (%s)\n", mode, n, ms / n, bytes / ms / 1e6,
+         cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
