@@ -32,23 +32,6 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   return r;
 }
 
-// Predicated refill: loads *p into v when pred != 0, else leaves v unchanged
-// (one predicated LDG, no branch, so the load is not tied to a basic block).
-__device__ __forceinline__ void ld_stream_if(uint4& v, const uint4* p, bool pred) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
-      "@q ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n\t}"
-      : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
-      : "l"(p), "r"((int)pred));
-}
-__device__ __forceinline__ void ld_stream_if(float4& v, const float4* p, bool pred) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
-      "@q ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];\n\t}"
-      : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w)
-      : "l"(p), "r"((int)pred));
-}
-
 // ---- packed fp32x2 (sm_100 FFMA2 / FADD2: two fp32 lanes per instruction) ----
 using f2 = unsigned long long;
 __device__ __forceinline__ f2 pk2(float lo, float hi) {

@@ -97,7 +97,10 @@ __device__ __forceinline__ void lockstep_accumulate(const ET* const (&rows)[NT],
     }
 }
 
-template <typename ET, int NT, int U, bool PF, bool LOSS, bool ENT0, int MATH, bool LS = false>
+// U / PF: the layout of the entropy (actor) row; UN / PFN: the layout of the
+// other rows (old / ref, or the rows of a pass without entropy).
+template <typename ET, int NT, int U, bool PF, bool LOSS, bool ENT0, int MATH, bool LS = false, int UN = U,
+          bool PFN = PF>
 __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel(const VocabArgs a) {
   __shared__ float red[2][kWarps][NT][3];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
           // ex2.approx.ftz flushed part of its mass to zero; NaN fails both.
           if (!(acc[k].s >= 0x1p-80f && acc[k].s < 0x1p100f)) {
             acc_init(acc[k]);
-            stream_accumulate<kThreads, ET, U, PF, false, MATH>(rows[k], a.V, acc[k]);
+            stream_accumulate<kThreads, ET, UN, PFN, false, MATH>(rows[k], a.V, acc[k]);
           }
         goto reduce;
       }
@@ -159,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
           }
         }
       } else
-        stream_accumulate<kThreads, ET, U, PF, false, MATH>(rp, a.V, acc[k]);
+        stream_accumulate<kThreads, ET, UN, PFN, false, MATH>(rp, a.V, acc[k]);
     }
   reduce:
 #pragma unroll
@@ -180,9 +183,10 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
   }
 }
 
-template <typename ET, int NT, bool LOSS, bool ENT0, int MATH, int U, bool PF, bool LS = false>
+template <typename ET, int NT, bool LOSS, bool ENT0, int MATH, int U, bool PF, bool LS = false, int UN = U,
+          bool PFN = PF>
 cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
-  auto kern = vocab_ldg_kernel<ET, NT, U, PF, LOSS, ENT0, MATH, LS>;
+  auto kern = vocab_ldg_kernel<ET, NT, U, PF, LOSS, ENT0, MATH, LS, UN, PFN>;
   const int64_t nrows = (int64_t)a.B * a.T;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0);
@@ -214,6 +218,12 @@ cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
 #ifndef RLO_BF16_PF
 #define RLO_BF16_PF true
 #endif
+#ifndef RLO_BF16_UN
+#define RLO_BF16_UN RLO_BF16_U
+#endif
+#ifndef RLO_BF16_PFN
+#define RLO_BF16_PFN RLO_BF16_PF
+#endif
 #ifndef RLO_BF16_SHORT_MATH
 #define RLO_BF16_SHORT_MATH 6
 #endif
@@ -227,7 +237,8 @@ cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
   } else {
     if constexpr (NT == 3 && LOSS)
       if (a.V < kLongRowV) return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_SHORT_MATH, 2, false, true>(a, num_sms, s);
-    return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF>(a, num_sms, s);
+    return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, false, RLO_BF16_UN, RLO_BF16_PFN>(
+        a, num_sms, s);
   }
 }
 

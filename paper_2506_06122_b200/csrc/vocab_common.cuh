@@ -337,66 +337,6 @@ __device__ __forceinline__ void acc_scalar(const ET* p, Acc& a) {
   if (ENT) a.w += w;
 }
 
-// Lazy-max streaming with in-place prefetch (RLO_BF16_STREAM=1): every vector
-// register is refilled with the next batch's vector right after its words
-// were unpacked (a predicated load: nothing is read past the last batch), so
-// the next batch is in flight during this batch's math without a second
-// register set and its copy-forward (16 MOVs per batch of 32 bf16; a
-// ping-pong pair of sets spills at 64 registers).  A batch that fails the lazy
-// test has already lost its registers to the next batch, so it is re-read (an
-// L2 hit) and redone the exact way -- rare: a thread's first batch of a row
-// takes the exact path directly, later ones only when an element lands ~27
-// log2 units above the running max (or is not finite).  The vectors past the
-// last full batch go one at a time (no padded batch).
-template <int NTH, typename ET, int U, bool ENT, int MATHG>
-__device__ __forceinline__ void stream_reload(const typename Vec<ET>::V* __restrict__ vrow, int nfull, int nvec,
-                                              Acc& a) {
-  using VT = Vec<ET>;
-  using VV = typename VT::V;
-  constexpr int kStep = NTH * U;
-  constexpr int kExact = MATHG & ~kMathLazy;
-  const int tid = threadIdx.x;
-  const VV* __restrict__ p = vrow + tid;
-  const f2 L2 = pk2(kL2E, kL2E);
-  if (nfull > 0) {
-    VV v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = ld_stream(p + u * NTH);
-    for (int base = 0; base < nfull; base += kStep) {
-      const bool more = base + kStep < nfull;
-      const VV* __restrict__ nxt = p + base + kStep;
-      const bool lazy = a.mL > kLazyMin;  // the thread's state holds a real max
-      if (!lazy) acc_rescale<ENT>(a, VT::template chunk_max<U>(v));
-      const f2 nmL = pk2(-a.mL, -a.mL);
-      f2 s0 = 0, s1 = 0, w0 = 0, w1 = 0;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const VV cur = v[u];
-        ld_stream_if(v[u], nxt + u * NTH, more);
-        VT::template vec_sums<ENT, kExact>(cur, u, L2, nmL, s0, s1, w0, w1);
-      }
-      const float cs = hsum2(s0, s1);
-      if (!lazy || cs < kLazyCap) {  // inf / NaN fail the test and are redone below
-        a.s += cs;
-        if (ENT) a.w += hsum2(w0, w1);
-      } else {
-        VV t[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) t[u] = ld_stream(p + base + u * NTH);
-        VT::template accumulate<U, ENT, kExact>(t, a);
-      }
-    }
-  }
-  for (int idx = nfull + tid; idx < nvec; idx += NTH) {
-    const VV one[1] = {ld_stream(vrow + idx)};
-    VT::template accumulate<1, ENT, MATHG>(one, a);
-  }
-}
-
-#ifndef RLO_BF16_STREAM
-#define RLO_BF16_STREAM 0
-#endif
-
 // One row (or row slice) of V elements streamed by NTH threads with U 128-bit
 // loads in flight per thread.  A row that does not start on a 16-byte
 // boundary (e.g. V = 50257 in a contiguous tensor) takes its first few
@@ -416,11 +356,6 @@ __device__ __forceinline__ void stream_accumulate(const ET* __restrict__ row, in
   V -= head;
   const int nvec = V / VT::kElems;
   const int nfull = nvec / kStep * kStep;
-  if constexpr (PF && (MATH & kMathLazy) != 0 && RLO_BF16_STREAM == 1) {
-    stream_reload<NTH, ET, U, ENT, MATH>(reinterpret_cast<const VV*>(row), nfull, nvec, a);
-    for (int i = nvec * VT::kElems + tid; i < V; i += NTH) acc_scalar<ET, ENT>(row + i, a);  // scalar tail
-    return;
-  }
   const VV* __restrict__ vrow = reinterpret_cast<const VV*>(row) + tid;
   if (PF) {
     if (nfull > 0) {
