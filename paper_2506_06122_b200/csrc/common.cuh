@@ -32,6 +32,19 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   return r;
 }
 
+// sm_100 256-bit streaming load (LDG.E.NA.256): 32 contiguous bytes into two
+// 16-byte vectors; p must be 32-byte aligned.
+__device__ __forceinline__ void ld_stream256(const uint4* p, uint4& a, uint4& b) {
+  asm("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+      : "l"(p));
+}
+__device__ __forceinline__ void ld_stream256(const float4* p, float4& a, float4& b) {
+  asm("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+      : "l"(p));
+}
+
 // ---- packed fp32x2 (sm_100 FFMA2 / FADD2: two fp32 lanes per instruction) ----
 using f2 = unsigned long long;
 __device__ __forceinline__ f2 pk2(float lo, float hi) {

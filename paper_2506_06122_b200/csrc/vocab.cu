@@ -152,6 +152,8 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
       if (k == 0 && ENT0) {
         if (RLO_ENT_GUARD_ALWAYS || sizeof(ET) == 4) {  // fp32 rows are memory-bound: one guarded body
           stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, acc[k]);
+        } else if constexpr ((MATH & kMathDeferred) != 0) {
+          stream_checked<kThreads, ET, U, PF, true, MATH>(rp, a.V, acc[k]);
         } else {
           stream_accumulate<kThreads, ET, U, PF, true, MATH>(rp, a.V, acc[k]);
           if (!(isfinite(acc[k].s) && isfinite(acc[k].w))) {
@@ -161,8 +163,11 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
             stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, acc[k]);
           }
         }
-      } else
+      } else if constexpr ((MATH & kMathDeferred) != 0) {
+        stream_checked<kThreads, ET, UN, PFN, false, MATH>(rp, a.V, acc[k]);
+      } else {
         stream_accumulate<kThreads, ET, UN, PFN, false, MATH>(rp, a.V, acc[k]);
+      }
     }
   reduce:
 #pragma unroll

@@ -140,6 +140,17 @@ constexpr int kMathNoMax = 0x200;
 // (H = log2 s - w/s holds for every offset) -- so this drops the per-element
 // max (one HMNMX2 / FMNMX per pair) from almost every chunk.
 constexpr int kMathLazy = 0x400;
+// kMathDeferred: the offset is the max of the thread's FIRST batch of the
+// row (exact path) and every later batch is summed against it with no check
+// at all -- no per-batch max, test or branch; the batch sums go into packed
+// accumulators.  Valid for the same reason as the lazy max (any offset that
+// keeps the terms finite gives the same lse and entropy); a thread whose
+// share ends with s >= kDeferCap or a non-finite s / w (an element ~110 log2
+// units above that offset: MUFU lanes overflow to inf, polynomial lanes clamp
+// at 2^127; or -inf logits in the entropy row) is redone the exact way by the
+// caller (stream_checked).
+constexpr int kMathDeferred = 0x800;
+constexpr float kDeferCap = 0x1p110f;
 constexpr float kLazyCap = 4294967296.0f;  // 2^32
 constexpr float kLazyMin = -1.0e29f;      // mL above this holds a real max (init is kNegInit * kL2E)
 
@@ -337,6 +348,16 @@ __device__ __forceinline__ void acc_scalar(const ET* p, Acc& a) {
   if (ENT) a.w += w;
 }
 
+// 256-bit loads (sm_100 LDG.256) in the prefetching layout (the bf16 default):
+// +0.5-0.8% on cfg3 (profiles/r2_vocab_ab.txt); in the non-prefetching
+// layout (the fp32 default, U = 8) they lost 3.5% on cfg2 and stay off.
+#ifndef RLO_LDG256
+#define RLO_LDG256 1
+#endif
+#ifndef RLO_LDG256_NOPF
+#define RLO_LDG256_NOPF 0
+#endif
+
 // One row (or row slice) of V elements streamed by NTH threads with U 128-bit
 // loads in flight per thread.  A row that does not start on a 16-byte
 // boundary (e.g. V = 50257 in a contiguous tensor) takes its first few
@@ -357,7 +378,77 @@ __device__ __forceinline__ void stream_accumulate(const ET* __restrict__ row, in
   const int nvec = V / VT::kElems;
   const int nfull = nvec / kStep * kStep;
   const VV* __restrict__ vrow = reinterpret_cast<const VV*>(row) + tid;
-  if (PF) {
+  if constexpr (PF && (MATH & kMathDeferred) != 0) {
+    constexpr int kExact = MATH & ~kMathDeferred;
+    const f2 L2 = pk2(kL2E, kL2E);
+    f2 nmL = pk2(-a.mL, -a.mL);
+    f2 S0 = 0, S1 = 0, W0 = 0, W1 = 0;
+    auto batch = [&](const VV (&v)[U]) {
+      if (!(a.mL > kLazyMin)) {  // the thread's first batch of the row: exact, sets the offset
+        VT::template accumulate<U, ENT, kExact>(v, a);
+        nmL = pk2(-a.mL, -a.mL);
+        return;
+      }
+      f2 c0 = 0, c1 = 0, d0 = 0, d1 = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) VT::template vec_sums<ENT, kExact>(v[u], u, L2, nmL, c0, c1, d0, d1);
+      S0 = fadd2(S0, c0);
+      S1 = fadd2(S1, c1);
+      if (ENT) {
+        W0 = fadd2(W0, d0);
+        W1 = fadd2(W1, d1);
+      }
+    };
+    if (nfull > 0) {
+      VV cur[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) cur[u] = ld_stream(vrow + u * NTH);
+      for (int base = kStep; base < nfull; base += kStep) {
+        VV nxt[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) nxt[u] = ld_stream(vrow + base + u * NTH);
+        batch(cur);
+#pragma unroll
+        for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+      }
+      batch(cur);
+    }
+    a.s += hsum2(S0, S1);  // before the exact tail, which may rescale the state
+    if (ENT) a.w += hsum2(W0, W1);
+  } else if (PF && RLO_LDG256 && (U % 2) == 0) {
+    // 256-bit loads: thread tid takes the vector pairs (2 tid, 2 tid + 1) of
+    // each 2*NTH-vector group of the batch -- one LDG.256 per pair, half the
+    // load instructions, a warp reads 1 KB contiguous per load.  Rows whose
+    // aligned body does not start on 32 bytes take the 16-byte layout below.
+    if (nfull > 0 && (reinterpret_cast<uintptr_t>(row) & 31u) == 0) {
+      const VV* __restrict__ prow = reinterpret_cast<const VV*>(row) + 2 * tid;
+      VV cur[U];
+#pragma unroll
+      for (int u = 0; u < U; u += 2) ld_stream256(prow + u * NTH, cur[u], cur[u + 1]);
+      for (int base = kStep; base < nfull; base += kStep) {
+        VV nxt[U];
+#pragma unroll
+        for (int u = 0; u < U; u += 2) ld_stream256(prow + base + u * NTH, nxt[u], nxt[u + 1]);
+        VT::template accumulate<U, ENT, MATH>(cur, a);
+#pragma unroll
+        for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+      }
+      VT::template accumulate<U, ENT, MATH>(cur, a);
+    } else if (nfull > 0) {
+      VV cur[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) cur[u] = ld_stream(vrow + u * NTH);
+      for (int base = kStep; base < nfull; base += kStep) {
+        VV nxt[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) nxt[u] = ld_stream(vrow + base + u * NTH);
+        VT::template accumulate<U, ENT, MATH>(cur, a);
+#pragma unroll
+        for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+      }
+      VT::template accumulate<U, ENT, MATH>(cur, a);
+    }
+  } else if (PF) {
     if (nfull > 0) {
       VV cur[U];
 #pragma unroll
@@ -372,6 +463,14 @@ __device__ __forceinline__ void stream_accumulate(const ET* __restrict__ row, in
       }
       VT::template accumulate<U, ENT, MATH>(cur, a);
     }
+  } else if (RLO_LDG256_NOPF && (U % 2) == 0 && (reinterpret_cast<uintptr_t>(row) & 31u) == 0) {
+    const VV* __restrict__ prow = reinterpret_cast<const VV*>(row) + 2 * tid;  // 256-bit pairs, as above
+    for (int base = 0; base < nfull; base += kStep) {
+      VV v[U];
+#pragma unroll
+      for (int u = 0; u < U; u += 2) ld_stream256(prow + base + u * NTH, v[u], v[u + 1]);
+      VT::template accumulate<U, ENT, MATH>(v, a);
+    }
   } else {
     for (int base = 0; base < nfull; base += kStep) {  // full batches: unpredicated loads
       VV v[U];
@@ -380,16 +479,36 @@ __device__ __forceinline__ void stream_accumulate(const ET* __restrict__ row, in
       VT::template accumulate<U, ENT, MATH>(v, a);
     }
   }
-  if (nfull < nvec) {  // last partial batch
+  if (nfull < nvec) {  // last partial batch (exact path under kMathDeferred)
     VV v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int idx = nfull + u * NTH + tid;
       v[u] = idx < nvec ? ld_stream(vrow - tid + idx) : VT::fill();
     }
-    VT::template accumulate<U, ENT, MATH>(v, a);
+    VT::template accumulate<U, ENT, MATH & ~kMathDeferred>(v, a);
   }
   for (int i = nvec * VT::kElems + tid; i < V; i += NTH) acc_scalar<ET, ENT>(row + i, a);  // scalar tail
+}
+
+// stream_accumulate plus the deferred check: a share whose state left the
+// safe range (see kMathDeferred) is redone the exact way (entropy rows
+// guarded); the redo re-reads the thread's share, which the stream has just
+// brought through L2.
+template <int NTH, typename ET, int U, bool PF, bool ENT, int MATH>
+__device__ __forceinline__ void stream_checked(const ET* __restrict__ row, int V, Acc& a) {
+  stream_accumulate<NTH, ET, U, PF, ENT, MATH>(row, V, a);
+  constexpr bool kDeferred = (MATH & kMathDeferred) != 0;
+  if constexpr (kDeferred || ENT) {
+    // deferred: overflowed or not finite; lazy / exact entropy rows: -inf
+    // logits make the unguarded e * t = 0 * -inf NaN (w - w != 0 for inf / NaN)
+    const bool bad = kDeferred ? (!(a.s < kDeferCap) || (ENT && !(a.w - a.w == 0.f)))
+                               : !(isfinite(a.s) && isfinite(a.w));
+    if (bad) {
+      acc_init(a);
+      stream_accumulate<NTH, ET, U, PF, ENT, (MATH & ~kMathDeferred) | (ENT ? kMathGuard : 0)>(row, V, a);
+    }
+  }
 }
 
 struct RowResult {
