@@ -100,6 +100,20 @@ __global__ void __launch_bounds__(256, 4) probe_kernel(const uint4* t0, const ui
   if (tid == 0 && red[0] == 1234.5f) out[0] = red[1];  // keep the work
 }
 
+// Random bf16 logits in [-8, 8) (a counter hash), like the bench's synthetic
+// rows: the bit toggling of the data path matters for power.
+__global__ void fill_random(uint32_t* p, int64_t n, uint32_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = (uint64_t)i * 0x9E3779B97F4A7C15ull + seed;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    const float lo = ((float)(uint32_t)(z & 0xFFFFFF) / 16777216.0f) * 16.0f - 8.0f;
+    const float hi = ((float)(uint32_t)((z >> 24) & 0xFFFFFF) / 16777216.0f) * 16.0f - 8.0f;
+    p[i] = (__float_as_uint(lo) >> 16) | (__float_as_uint(hi) & 0xFFFF0000u);
+  }
+}
+
 int main(int argc, char** argv) {
   const int mode = argc > 1 ? atoi(argv[1]) : 0;
   const double secs = argc > 2 ? atof(argv[2]) : 6.0;
@@ -110,7 +124,10 @@ int main(int argc, char** argv) {
   uint4* t[3];
   for (int k = 0; k < 3; ++k) {
     cudaMalloc(&t[k], rows * rb);
-    cudaMemset(t[k], 0x3F + k, rows * rb);  // bf16 words ~0.5..1.5: finite exponentials
+    if (argc > 3 && atoi(argv[3]) == 1)
+      fill_random<<<1184, 256>>>(reinterpret_cast<uint32_t*>(t[k]), rows * rb / 4, 17u + k);
+    else
+      cudaMemset(t[k], 0x3F + k, rows * rb);  // bf16 words ~0.5..1.5: finite exponentials
   }
   float* out;
   cudaMalloc(&out, 4);
@@ -139,7 +156,8 @@ int main(int argc, char** argv) {
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   const double bytes = 3.0 * rows * (double)(nvec / 1024 * 1024) * 16 * n;
-  printf("power_probe mode=%d: %d launches, %.3f ms/launch, %.0f GB/s (%s)\n", mode, n, ms / n, bytes / ms / 1e6,
+  printf("power_probe mode=%d data=%s: %d launches, %.3f ms/launch, %.0f GB/s (%s)\n", mode,
+         (argc > 3 && atoi(argv[3]) == 1) ? "random" : "constant", n, ms / n, bytes / ms / 1e6,
          cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
