@@ -1,6 +1,6 @@
 // vocab_common.cuh — the online log-sum-exp state, per-dtype chunk math and
-// the per-row epilogue shared by the two vocab-pass kernels (vocab.cu: 128-bit
-// LDG streaming; vocab_tma.cu: TMA bulk-copy shared-memory ring).
+// the per-row epilogue of the vocab pass (vocab.cu) and the fused update pass
+// (fused.cu).
 //
 // State per (thread, tensor), in log2 units relative to the fp32 constant kL2E:
 //   mL = running max of z*kL2E (fp32-rounded), s = sum 2^(z*kL2E - mL),
@@ -102,8 +102,9 @@ __device__ __forceinline__ void acc_warp_reduce(Acc& a) {
 
 // ---- per-dtype 16-byte vector math -------------------------------------------
 //
-// MATH selects the per-element instruction mix (runtime-selected, see
-// vocab.cu: RLO_VOCAB_MATH; defaults per dtype):
+// MATH selects the per-element instruction mix (compile-time; the shipped
+// defaults per dtype are in vocab.cu: fp32 1, bf16 6 | kMathLazy, bf16 short
+// 3-tensor rows 6; the others are A/B options):
 //   0  scalar FFMA / MUFU.EX2 / FADD per element;
 //   1  packed: FFMA2 / FADD2 on element pairs, MUFU.EX2 per element;
 //   2  as 1, plus 1 of 4 element pairs of each non-entropy row through the
