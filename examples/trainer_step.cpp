@@ -110,6 +110,31 @@ int main() {
       return 1;
     }
 
+    // ---- the same step from host SampleBatch arrays (the reference-facing call):
+    //      one copy in, advantages over the whole batch, a callback per
+    //      micro-batch that names its logits (where the model forward would run)
+    std::vector<int32_t> htok((size_t)B * T);
+    CK(cudaMemcpy(htok.data(), d_tok, sizeof(int32_t) * htok.size(), cudaMemcpyDeviceToHost));
+    std::vector<float> hadv((size_t)B * T), hlp((size_t)B * T);
+    int calls = 0;
+    const rlo::UpdateStats st3 = obj.step_host_mb(
+        cfg, B, T, MB, lengths.data(), htok.data(), nullptr, nullptr, rewards.data(), nullptr,
+        [&](int32_t mb, int32_t b0, int32_t nb, rlo_logits* a, rlo_logits* o, rlo_logits* r) {
+          ++calls;
+          (void)mb;
+          (void)nb;
+          *a = view(0, b0);
+          *o = view(1, b0);
+          *r = view(2, b0);
+        },
+        nullptr, nullptr, hadv.data(), hlp.data(), s);
+    std::printf("host step: loss %.9f tokens %llu (%d micro-batch callbacks)\n", st3.loss,
+                (unsigned long long)st3.tokens, calls);
+    if (st3.loss != st.loss || st3.tokens != st.tokens || calls != B / MB) {
+      std::fprintf(stderr, "host-buffer step disagrees with the device step\n");
+      return 1;
+    }
+
     // ---- next rollout: sample one token per sequence with its untempered log-prob
     std::vector<uint64_t> keys(B), pos(B, 0);
     for (int b = 0; b < B; ++b) keys[b] = rlo_sample_key(("sample-" + std::to_string(b)).c_str());

@@ -16,6 +16,8 @@
 #pragma once
 
 #include <cstdint>
+#include <exception>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -171,6 +173,51 @@ class Objective {
                        const float* weight, void* grad, int32_t grad_dtype, int64_t grad_row_stride,
                        void* stream = nullptr) {
     check(rlo_logits_backward(h_, &batch, &logits, lse, dlogp, weight, grad, grad_dtype, grad_row_stride, stream));
+  }
+  // The whole step from host SampleBatch arrays (rlo_objective_step_host).
+  UpdateStats step_host(const TrainConfig& cfg, int32_t B, int32_t T, const int32_t* lengths, const int32_t* tokens,
+                        const uint8_t* mask, const float* rewards_tok, const float* rewards_seq, const float* values,
+                        const rlo_logits& actor, const rlo_logits* old_logits, const rlo_logits* ref_logits,
+                        const float* old_logp, const float* ref_logp, float* adv_out, float* logp_out,
+                        void* stream = nullptr) {
+    UpdateStats st{};
+    check(rlo_objective_step_host(h_, &cfg, B, T, lengths, tokens, mask, rewards_tok, rewards_seq, values, &actor,
+                                  old_logits, ref_logits, old_logp, ref_logp, adv_out, logp_out, &st, stream));
+    return st;
+  }
+  // Micro-batched form (rlo_objective_step_host_mb): `logits(mb, seq_begin,
+  // n_seqs, actor, old, ref)` names each micro-batch's device logits (run the
+  // model forward there); an exception thrown by it aborts the step and is
+  // rethrown here.
+  using LogitsFn = std::function<void(int32_t mb, int32_t seq_begin, int32_t n_seqs, rlo_logits* actor,
+                                      rlo_logits* old_logits, rlo_logits* ref_logits)>;
+  UpdateStats step_host_mb(const TrainConfig& cfg, int32_t B, int32_t T, int32_t mb_seqs, const int32_t* lengths,
+                           const int32_t* tokens, const uint8_t* mask, const float* rewards_tok,
+                           const float* rewards_seq, const float* values, const LogitsFn& logits,
+                           const float* old_logp, const float* ref_logp, float* adv_out, float* logp_out,
+                           void* stream = nullptr) {
+    struct Ctx {
+      const LogitsFn* fn;
+      std::exception_ptr err;
+    } ctx{&logits, nullptr};
+    auto tramp = [](void* user, int32_t mb, int32_t b0, int32_t nb, rlo_logits* a, rlo_logits* o,
+                    rlo_logits* r) -> rlo_status {
+      auto* c = static_cast<Ctx*>(user);
+      try {
+        (*c->fn)(mb, b0, nb, a, o, r);
+        return RLO_OK;
+      } catch (...) {
+        c->err = std::current_exception();
+        return RLO_ERR_INPUT;
+      }
+    };
+    UpdateStats st{};
+    const rlo_status rc = rlo_objective_step_host_mb(h_, &cfg, B, T, mb_seqs, lengths, tokens, mask, rewards_tok,
+                                                     rewards_seq, values, tramp, &ctx, old_logp, ref_logp, adv_out,
+                                                     logp_out, &st, stream);
+    if (ctx.err) std::rethrow_exception(ctx.err);
+    check(rc);
+    return st;
   }
   void sync(void* stream = nullptr) { check(rlo_sync(h_, stream)); }
   rlo_handle* get() const { return h_; }
