@@ -1,1 +1,3 @@
-bash tools/probes/power_probe.sh 2>&1 | tee gpurun_out/r2_power_probe2.txt
+./build/trainer_step 2>&1 | tail -5
+./build/integration_test | tail -2
+bash tools/ab_bench.sh h 2 head nopf5 nopf6 | tee gpurun_out/r2j_ab.txt

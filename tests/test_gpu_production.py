@@ -330,6 +330,42 @@ def test_bf16_lockstep_offsets(env, off_old, off_ref):
             assert_close(outs["entropy"].cpu().numpy().ravel()[m], ent[m], what="entropy")
 
 
+@pytest.mark.parametrize("pad", [8, 1, 16])
+def test_bf16_row_alignments(env, pad):
+    """The bf16 pass reads 32-byte pairs (LDG.256) when a row's aligned body
+    starts on 32 bytes and 16-byte vectors otherwise: a row stride of V + 8
+    alternates the two layouts row by row, V + 1 also shifts the scalar head,
+    V + 16 keeps every row 32-byte aligned.  P = 3 loss pass and
+    forward_logprobs against the oracle."""
+    torch, rlo, obj = env
+    rng = np.random.default_rng(100 + pad)
+    B, T, V = 2, 3, QWEN_V
+    lengths = np.array([3, 2], np.int32)
+    rows = [rng.standard_normal((B * T, V)).astype(np.float32) * 3 for _ in range(3)]
+    dev_rows, host_rows = [], []
+    for r in rows:
+        full = torch.zeros(B * T, V + pad, dtype=torch.bfloat16)
+        full[:, :V] = torch.from_numpy(r).to(torch.bfloat16)
+        dev_rows.append(full.cuda()[:, :V])
+        host_rows.append(full[:, :V].contiguous().view(torch.int16).numpy().view(np.uint16))
+    tokens = rng.integers(0, V, (B, T)).astype(np.int32)
+    K, L = dev(torch, tokens), dev(torch, lengths)
+    cfg = rlo.TrainConfig(kl_coef=0.01, kl_estimator="k2")
+    outs = obj.ppo_gradient(cfg, K, L, dev_rows[0], dev(torch, np.zeros((B, T), np.float32)),
+                            old_logits=dev_rows[1], ref_logits=dev_rows[2],
+                            outputs=("logp", "old_logp", "ref_logp", "entropy"))
+    obj.merge_gradients(cfg)
+    m = valid_mask(B, T, lengths)
+    for name, k in (("logp", 0), ("old_logp", 1), ("ref_logp", 2)):
+        want, ent, _ = O.forward_logprobs(host_rows[k], O.BF16, V, V, B, T, lengths, tokens)
+        assert_close(outs[name].cpu().numpy().ravel()[m], want[m], what=f"{name} pad {pad}")
+        if k == 0:
+            assert_close(outs["entropy"].cpu().numpy().ravel()[m], ent[m], what="entropy")
+    fl = obj.forward_logprobs(dev_rows[2], K, L, entropy=False)
+    want, _, _ = O.forward_logprobs(host_rows[2], O.BF16, V, V, B, T, lengths, tokens)
+    assert_close(fl["logp"].cpu().numpy().ravel()[m], want[m], what="forward_logprobs")
+
+
 # ---- every shipped forward_logprobs instantiation --------------------------------------------------
 
 @pytest.mark.parametrize("dt,V", [("f32", 32000), ("bf16", QWEN_V), ("bf16", 4096)])
