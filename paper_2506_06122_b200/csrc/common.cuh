@@ -34,8 +34,21 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
 
 // sm_100 256-bit streaming load (LDG.E.NA.256): 32 contiguous bytes into two
 // 16-byte vectors; p must be 32-byte aligned.
+// RLO_LDG256_HINT (A/B): 1 = .L2::evict_first, 2 = .L2::256B prefetch, 3 = both.
+#ifndef RLO_LDG256_HINT
+#define RLO_LDG256_HINT 0
+#endif
+#if RLO_LDG256_HINT == 1
+#define RLO_LD256_OP "ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32"
+#elif RLO_LDG256_HINT == 2
+#define RLO_LD256_OP "ld.global.nc.L1::no_allocate.L2::256B.v8.b32"
+#elif RLO_LDG256_HINT == 3
+#define RLO_LD256_OP "ld.global.nc.L1::no_allocate.L2::evict_first.L2::256B.v8.b32"
+#else
+#define RLO_LD256_OP "ld.global.nc.L1::no_allocate.v8.b32"
+#endif
 __device__ __forceinline__ void ld_stream256(const uint4* p, uint4& a, uint4& b) {
-  asm("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+  asm(RLO_LD256_OP " {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
       : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
       : "l"(p));
 }
