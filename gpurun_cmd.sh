@@ -1,1 +1,1 @@
-bash tools/ab_bench.sh i 2 head h1 h2 h3 | tee gpurun_out/r2l_ab.txt
+MODES="0:1,4:1,0:1,4:1" bash tools/probes/power_probe.sh 2>&1 | tee gpurun_out/r2_power_probe3.txt

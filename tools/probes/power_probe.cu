@@ -100,6 +100,28 @@ __global__ void __launch_bounds__(256, 4) probe_kernel(const uint4* t0, const ui
   if (tid == 0 && red[0] == 1234.5f) out[0] = red[1];  // keep the work
 }
 
+// Mode 4: the memory system alone (XOR) with a grid-linear sweep instead of
+// one row per CTA: every batch step the whole grid reads one contiguous block
+// (CTA b takes the b-th 16 KB of it), so the addresses in flight form a few
+// sequential streams instead of #CTA streams spaced a row apart.
+__global__ void __launch_bounds__(256, 4) sweep_kernel(const uint4* t0, const uint4* t1, const uint4* t2,
+                                                       int64_t nvec_total, float* out) {
+  const uint4* ts[3] = {t0, t1, t2};
+  const int tid = threadIdx.x;
+  uint32_t acc = 0;
+  const int64_t step = (int64_t)gridDim.x * 1024;
+#pragma unroll 1
+  for (int k = 0; k < 3; ++k)
+    for (int64_t base = (int64_t)blockIdx.x * 1024; base + 1024 <= nvec_total; base += step) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = ld_stream(ts[k] + base + u * 256 + tid);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+    }
+  if (acc == 0x12345678u) out[0] = 1.f;
+}
+
 // Random bf16 logits in [-8, 8) (a counter hash), like the bench's synthetic
 // rows: the bit toggling of the data path matters for power.
 __global__ void fill_random(uint32_t* p, int64_t n, uint32_t seed) {
@@ -136,7 +158,8 @@ int main(int argc, char** argv) {
       case 0: probe_kernel<0><<<sms * 4, 256>>>(t[0], t[1], t[2], rows, nvec, out); break;
       case 1: probe_kernel<1><<<sms * 4, 256>>>(t[0], t[1], t[2], rows, nvec, out); break;
       case 2: probe_kernel<2><<<sms * 4, 256>>>(t[0], t[1], t[2], rows, nvec, out); break;
-      default: probe_kernel<3><<<sms * 4, 256>>>(t[0], t[1], t[2], rows, nvec, out); break;
+      case 3: probe_kernel<3><<<sms * 4, 256>>>(t[0], t[1], t[2], rows, nvec, out); break;
+      default: sweep_kernel<<<sms * 4, 256>>>(t[0], t[1], t[2], rows * (int64_t)nvec, out); break;
     }
   };
   for (int i = 0; i < 3; ++i) launch();

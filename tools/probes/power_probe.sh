@@ -3,8 +3,9 @@
 cd "$(dirname "$0")/../.."
 mkdir -p build gpurun_out
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/power_probe tools/probes/power_probe.cu || exit 1
-for md in "0 0" "0 1" "1 1" "2 1" "3 1" "2 0"; do
-  m=${md% *}; d=${md#* }
+# MODES: comma-separated mode:data pairs (data 0 = constant bytes, 1 = random bf16)
+for md in $(echo "${MODES:-0:0,0:1,1:1,2:1,3:1,2:0}" | tr ',' ' '); do
+  m=${md%:*}; d=${md#*:}
   nvidia-smi --query-gpu=clocks.sm,power.draw,clocks_event_reasons.sw_power_cap --format=csv,noheader,nounits -lms 100 > /tmp/pw_$m.csv &
   P=$!
   r=$(./build/power_probe $m 8 $d)
