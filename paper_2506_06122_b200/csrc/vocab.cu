@@ -229,6 +229,9 @@ cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
 #ifndef RLO_BF16_PFN
 #define RLO_BF16_PFN RLO_BF16_PF
 #endif
+#ifndef RLO_BF16_MATH_P1
+#define RLO_BF16_MATH_P1 RLO_BF16_MATH
+#endif
 #ifndef RLO_BF16_SHORT_MATH
 #define RLO_BF16_SHORT_MATH 6
 #endif
@@ -242,6 +245,8 @@ cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
   } else {
     if constexpr (NT == 3 && LOSS)
       if (a.V < kLongRowV) return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_SHORT_MATH, 2, false, true>(a, num_sms, s);
+    if constexpr (NT == 1 && LOSS && ENT0 && RLO_BF16_MATH_P1 != RLO_BF16_MATH)  // A/B: actor-only loss pass
+      return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH_P1, RLO_BF16_U, RLO_BF16_PF>(a, num_sms, s);
     return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, false, RLO_BF16_UN, RLO_BF16_PFN>(
         a, num_sms, s);
   }
