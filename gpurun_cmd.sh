@@ -1,1 +1,1 @@
-AB_P1=1 bash tools/ab_bench.sh j 2 head p1m4 p1m8 | tee gpurun_out/r2m_ab.txt
+MODES="2:1,5:1,6:1,2:1,5:1,6:1" bash tools/probes/power_probe.sh 2>&1 | tee gpurun_out/r2_power_probe4.txt

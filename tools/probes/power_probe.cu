@@ -9,6 +9,8 @@
 //   2 mufu    : 1 + MUFU.EX2 per element (sum of 2^t): the real pass's math
 //               without the online max / lazy check / polynomial lanes
 //   3 mufu+w  : 2 + the entropy FFMA2 on every element
+//   4 sweep   : 0 with a grid-linear address sweep instead of one row per CTA
+//   5 / 6     : 2 with the degree-4 FMA-pipe exp2 on 25% / 50% of the element pairs
 // The wrapper (tools/probes/power_probe.sh) samples SM clock and board power
 // with nvidia-smi while each mode runs.  Build:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/power_probe tools/probes/power_probe.cu
@@ -48,8 +50,30 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// degree-4 FMA-pipe 2^t for a pair, t clamped to [-126, 127] (the pass's polynomial lanes)
+__device__ __forceinline__ f2 poly2(f2 t) {
+  constexpr float kMagic = 12582912.0f;
+  float tl, th;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(tl), "=f"(th) : "l"(t));
+  tl = fminf(fmaxf(tl, -126.f), 127.f);
+  th = fminf(fmaxf(th, -126.f), 127.f);
+  const f2 tc = pk2(tl, th);
+  const f2 r = fadd2(tc, pk2(kMagic, kMagic));
+  const f2 j = fadd2(r, pk2(-kMagic, -kMagic));
+  const f2 f = ffma2(j, pk2(-1.0f, -1.0f), tc);
+  f2 p = ffma2(f, pk2(0x1.3a02ccp-7f, 0x1.3a02ccp-7f), pk2(0x1.c9fc46p-5f, 0x1.c9fc46p-5f));
+  p = ffma2(p, f, pk2(0x1.ec0378p-3f, 0x1.ec0378p-3f));
+  p = ffma2(p, f, pk2(0x1.62e12cp-1f, 0x1.62e12cp-1f));
+  p = ffma2(p, f, pk2(1.0f, 1.0f));
+  float pl, ph, rl, rh;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(pl), "=f"(ph) : "l"(p));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(rl), "=f"(rh) : "l"(r));
+  return pk2(__uint_as_float(__float_as_uint(rl) * 8388608u + __float_as_uint(pl)),
+             __uint_as_float(__float_as_uint(rh) * 8388608u + __float_as_uint(ph)));
+}
+
 template <int MODE>
-__device__ __forceinline__ void word(uint32_t x, f2 L2, f2 nm, f2& s, f2& w, uint32_t& acc) {
+__device__ __forceinline__ void word(uint32_t x, f2 L2, f2 nm, f2& s, f2& w, uint32_t& acc, bool poly = false) {
   if (MODE == 0) {
     acc ^= x;
     return;
@@ -61,7 +85,7 @@ __device__ __forceinline__ void word(uint32_t x, f2 L2, f2 nm, f2& s, f2& w, uin
   }
   float tl, th;
   asm("mov.b64 {%0, %1}, %2;" : "=f"(tl), "=f"(th) : "l"(t));
-  const f2 e = pk2(ex2(tl), ex2(th));
+  const f2 e = poly ? poly2(t) : pk2(ex2(tl), ex2(th));
   s = fadd2(s, e);
   if (MODE == 3) w = ffma2(e, t, w);
 }
@@ -83,12 +107,13 @@ __global__ void __launch_bounds__(256, 4) probe_kernel(const uint4* t0, const ui
         uint4 v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) v[u] = ld_stream(row + base + u * 256);
+        constexpr int M = MODE >= 5 ? 2 : MODE;  // 5: mode 2 + polynomial on the .y words (25%); 6: .y and .w (50%)
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          word<MODE>(v[u].x, L2, nm, s, w, acc);
-          word<MODE>(v[u].y, L2, nm, s, w, acc);
-          word<MODE>(v[u].z, L2, nm, s, w, acc);
-          word<MODE>(v[u].w, L2, nm, s, w, acc);
+          word<M>(v[u].x, L2, nm, s, w, acc);
+          word<M>(v[u].y, L2, nm, s, w, acc, MODE >= 5);
+          word<M>(v[u].z, L2, nm, s, w, acc);
+          word<M>(v[u].w, L2, nm, s, w, acc, MODE == 6);
         }
       }
     }
@@ -159,6 +184,8 @@ int main(int argc, char** argv) {
       case 1: probe_kernel<1><<<sms * 4, 256>>>(t[0], t[1], t[2], rows, nvec, out); break;
       case 2: probe_kernel<2><<<sms * 4, 256>>>(t[0], t[1], t[2], rows, nvec, out); break;
       case 3: probe_kernel<3><<<sms * 4, 256>>>(t[0], t[1], t[2], rows, nvec, out); break;
+      case 5: probe_kernel<5><<<sms * 4, 256>>>(t[0], t[1], t[2], rows, nvec, out); break;
+      case 6: probe_kernel<6><<<sms * 4, 256>>>(t[0], t[1], t[2], rows, nvec, out); break;
       default: sweep_kernel<<<sms * 4, 256>>>(t[0], t[1], t[2], rows * (int64_t)nvec, out); break;
     }
   };
