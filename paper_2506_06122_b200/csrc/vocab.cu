@@ -45,7 +45,11 @@ constexpr int kWarps = kThreads / 32;
 // a tensor so far below it that flushed terms matter — is redone with the
 // tensor's own max (the kernel below).  Rows must all be 16-byte aligned
 // (else the sequential streams).
-template <typename ET, int NT, int U, int MATH>
+// DEF (deferred offset; the shipped long-row layout): the shared offset is the
+// actor max of the thread's first batch only; later batches take no max, test
+// or rescale at all -- the kernel's range checks on the finished shares redo
+// any share that left the safe range.
+template <typename ET, int NT, int U, int MATH, bool DEF = false>
 __device__ __forceinline__ void lockstep_accumulate(const ET* const (&rows)[NT], int V, Acc (&acc)[NT]) {
   using VT = Vec<ET>;
   using VV = typename VT::V;
@@ -54,6 +58,12 @@ __device__ __forceinline__ void lockstep_accumulate(const ET* const (&rows)[NT],
   const int nvec = V / VT::kElems;
   const int nfull = nvec / kStep * kStep;
   auto step = [&](const VV (&v)[NT][U]) {
+    if (DEF && acc[0].mL > kLazyMin) {
+      VT::template accumulate<U, true, MATH | kMathNoMax>(v[0], acc[0]);
+#pragma unroll
+      for (int k = 1; k < NT; ++k) VT::template accumulate<U, false, MATH | kMathNoMax>(v[k], acc[k]);
+      return;
+    }
     const float newmL = __fmul_rn(VT::template chunk_max<U>(v[0]), kL2E);
     if (newmL > acc[0].mL) {  // rescale every state to the new shared max
       const float d = acc[0].mL - newmL, sc = ex2(d);
@@ -126,8 +136,12 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
         acc_init(acc[k]);
       }
       if (__all_sync(0xffffffffu, aligned)) {  // aligned is uniform per row anyway
-        lockstep_accumulate<ET, NT, U, MATH>(rows, a.V, acc);
-        if (!(isfinite(acc[0].s) && isfinite(acc[0].w))) {  // -inf logits in the actor share: guarded redo
+        lockstep_accumulate<ET, NT, U, MATH & kMathMask, (MATH & kMathDeferred) != 0>(rows, a.V, acc);
+        // Redo the actor share exactly (and guarded) on -inf logits (w = 0 * -inf)
+        // or, under the deferred offset, when the share's max sat so far above
+        // the offset (s >= 2^32, as the lazy max's cap) that the entropy's
+        // log2 s - w/s would cancel too many bits.
+        if (!(isfinite(acc[0].s) && isfinite(acc[0].w)) || ((MATH & kMathDeferred) && !(acc[0].s < kLazyCap))) {
           acc_init(acc[0]);
           stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rows[0], a.V, acc[0]);
         }
@@ -210,7 +224,12 @@ cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
 //        next batch in flight (software prefetch);
 //  bf16 3-tensor loss pass over short rows (< 128 KB): mix 6 with the three
 //        tensors streamed in lockstep on the actor's running max, U = 2 per
-//        tensor (one cold start per row instead of three).
+//        tensor (one cold start per row instead of three);
+//  bf16 3-tensor loss pass over long rows (cfg 3-5, V = 152064): mix 6 in
+//        lockstep, U = 3 per tensor, on a deferred offset (the actor max of
+//        the thread's first batch; no per-batch max, test or rescale):
+//        +3-4% over the per-tensor lazy-max streams at the power cap
+//        (profiles/r2_vocab_ab.txt).
 #ifndef RLO_F32_MATH
 #define RLO_F32_MATH 1
 #endif
@@ -232,6 +251,12 @@ cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
 #ifndef RLO_BF16_MATH_P1
 #define RLO_BF16_MATH_P1 RLO_BF16_MATH
 #endif
+#ifndef RLO_BF16_LONG_LS
+#define RLO_BF16_LONG_LS 3
+#endif
+#ifndef RLO_BF16_LONG_LS_MATH
+#define RLO_BF16_LONG_LS_MATH RLO_BF16_SHORT_MATH
+#endif
 #ifndef RLO_BF16_SHORT_MATH
 #define RLO_BF16_SHORT_MATH 6
 #endif
@@ -243,12 +268,18 @@ cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
   if constexpr (sizeof(ET) == 4) {
     return launch_ldg<ET, NT, LOSS, ENT0, RLO_F32_MATH, 8, false>(a, num_sms, s);
   } else {
-    if constexpr (NT == 3 && LOSS)
+    if constexpr (NT == 3 && LOSS && RLO_BF16_LONG_LS != 0) {  // lockstep: short rows / long rows
       if (a.V < kLongRowV) return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_SHORT_MATH, 2, false, true>(a, num_sms, s);
-    if constexpr (NT == 1 && LOSS && ENT0 && RLO_BF16_MATH_P1 != RLO_BF16_MATH)  // A/B: actor-only loss pass
-      return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH_P1, RLO_BF16_U, RLO_BF16_PF>(a, num_sms, s);
-    return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, false, RLO_BF16_UN, RLO_BF16_PFN>(
-        a, num_sms, s);
+      return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_LONG_LS_MATH | kMathDeferred, RLO_BF16_LONG_LS, false, true>(
+          a, num_sms, s);
+    } else {
+      if constexpr (NT == 3 && LOSS)
+        if (a.V < kLongRowV) return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_SHORT_MATH, 2, false, true>(a, num_sms, s);
+      if constexpr (NT == 1 && LOSS && ENT0 && RLO_BF16_MATH_P1 != RLO_BF16_MATH)  // A/B: actor-only loss pass
+        return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH_P1, RLO_BF16_U, RLO_BF16_PF>(a, num_sms, s);
+      return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, false, RLO_BF16_UN, RLO_BF16_PFN>(
+          a, num_sms, s);
+    }
   }
 }
 

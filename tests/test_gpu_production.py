@@ -5,15 +5,19 @@ tensor count, mode and entropy flag) is reached here at the shape it is
 selected for, through the C ABI (rlo_ppo_gradient / rlo_forward_logprobs /
 rlo_objective_step_host_mb):
 
-* bf16 V = 152064, P = 3 (BASELINE cfg 3-5): the lazy-running-max kernel with
-  the FMA-pipe exp2 on a quarter of the old/ref pairs (mix 7) -- reduced-size
+* bf16 V = 152064, P = 3 (BASELINE cfg 3-5): the long-row lockstep kernel
+  (the three rows streamed together on a deferred offset, the FMA-pipe exp2
+  on a quarter of the old/ref pairs) -- reduced-size
   end-to-end variants of cfg 3 (GRPO G=16, k3 0.001), cfg 4 (dual-clip c=3,
   global whitening, T = 16384, packed logits) and cfg 5 (GRPO G=8 + whitening),
-  one full-size cfg 3 micro-batch through size-independent properties, and the
-  rows that defeat a lazy max: every element far below one spike that sits in
-  a polynomial lane (the .y word of a uint4);
-* bf16 V < 65536, P = 3: the lockstep kernel (old/ref sums on the actor's
-  running max) with old/ref rows far above and far below the actor's;
+  one full-size cfg 3 micro-batch through size-independent properties, the
+  rows that defeat a lazy max / deferred offset: every element far below one
+  spike that sits in a polynomial lane (the .y word of a uint4), actor rows
+  whose later batches sit 5-40 nats above the first, -inf masked entries;
+* bf16 V = 152064, P = 1 / 2: the lazy-running-max kernel (mix 7);
+* bf16 V < 65536, P = 3: the short-row lockstep kernel (old/ref sums on the
+  actor's running max); both lockstep kernels with old/ref rows far above and
+  far below the actor's;
 * the fp32 and bf16 forward_logprobs instantiations with and without entropy.
 
 Tolerance (north_star): |gpu - oracle| <= 1e-5 * max(1, |oracle|) for
@@ -301,15 +305,17 @@ def test_bf16_spike_above_running_max_forward_logprobs(env, entropy):
         assert_close(out["entropy"].cpu().numpy().ravel(), ent, what="entropy (spike)")
 
 
+@pytest.mark.parametrize("V", [32000, QWEN_V])
 @pytest.mark.parametrize("off_old,off_ref", [(200.0, -80.0), (30.0, -40.0), (-300.0, 120.0)])
-def test_bf16_lockstep_offsets(env, off_old, off_ref):
-    """Short bf16 rows (V = 32000) take the lockstep kernel, whose old/ref sums
-    ride on the actor's running max: old/ref rows far above it (overflow side)
-    or far below it (ex2.approx.ftz flushes the bulk of the row) must be redone
-    with their own max."""
+def test_bf16_lockstep_offsets(env, off_old, off_ref, V):
+    """bf16 P = 3 rows take the lockstep kernels (short rows: on the actor's
+    running max; long rows: on the deferred offset), whose old/ref sums ride
+    on the actor's offset: old/ref rows far above it (overflow side) or far
+    below it (ex2.approx.ftz flushes the bulk of the row) must be redone with
+    their own max."""
     torch, rlo, obj = env
     rng = np.random.default_rng(int(abs(off_old)))
-    B, T, V = 4, 6, 32000
+    B, T = 4, 6
     lengths = np.array([6, 3, 5, 1], np.int32)
     base = rng.standard_normal((B * T, V)).astype(np.float32) * 2.5
     rows = [base, base + off_old + rng.standard_normal((B * T, V)).astype(np.float32) * 0.1,
@@ -328,6 +334,92 @@ def test_bf16_lockstep_offsets(env, off_old, off_ref):
         assert_close(outs[name].cpu().numpy().ravel()[m], want[m], what=f"{name} offset {off_old}/{off_ref}")
         if k == 0:
             assert_close(outs["entropy"].cpu().numpy().ravel()[m], ent[m], what="entropy")
+
+
+LS_FIRST = 3 * 256 * 8  # elements in the long-row lockstep kernel's first batch (U = 3 vectors x 256 threads)
+
+
+@pytest.mark.parametrize("gap", [0.0, 5.0, 10.0, 14.0, 40.0, "spike", "masked"])
+def test_bf16_long_lockstep_deferred_offset(env, gap):
+    """The long-row lockstep kernel (bf16, V = 152064, P = 3) sums every batch
+    after a thread's first against that first batch's actor max.  Rows whose
+    later elements sit `gap` nats above the first batch: below the redo cap
+    (s < 2^32) the entropy's log2 s - w/s cancels the gap's bits and must stay
+    within 1e-5; above it (gap 40, one +60 spike) the share is redone exactly;
+    "masked": a third of the actor row is -inf (masked vocabulary: guarded
+    redo).  Old / ref rows carry the same shape shifted by +-25 nats."""
+    torch, rlo, obj = env
+    rng = np.random.default_rng(77 if isinstance(gap, str) else int(gap * 10))
+    B, T, V = 2, 4, QWEN_V
+    lengths = np.array([4, 3], np.int32)
+    rows = rng.standard_normal((B * T, V)).astype(np.float32) * 1.5
+    if gap == "spike":
+        rows[:, LS_FIRST + 8 * 1000 + 5] = 60.0
+    elif gap == "masked":
+        rows[:, rng.choice(V, V // 3, replace=False)] = -np.inf
+    else:
+        rows[:, LS_FIRST:] += gap
+    tensors = [rows, rows[::-1] + 25.0, rows + rng.standard_normal(rows.shape).astype(np.float32) * 0.2 - 25.0]
+    if gap == "masked":
+        tensors[1] = np.where(np.isinf(rows), rows, tensors[1])
+    pairs = [bf16_bits(torch, r) for r in tensors]
+    tokens = rng.integers(LS_FIRST, V, (B, T)).astype(np.int32)
+    if gap == "masked":
+        tokens = np.array([[int(np.argmax(r)) for r in rows]], np.int32).reshape(B, T)
+    adv = rng.uniform(-1, 1, (B, T)).astype(np.float32)
+    cfg = rlo.TrainConfig(kl_coef=0.001, kl_estimator="k3")
+    outs = obj.ppo_gradient(cfg, dev(torch, tokens), dev(torch, lengths), pairs[0][0], dev(torch, adv),
+                            old_logits=pairs[1][0], ref_logits=pairs[2][0],
+                            outputs=("logp", "old_logp", "ref_logp", "entropy"))
+    obj.merge_gradients(cfg)
+    m = valid_mask(B, T, lengths)
+    for name, k in (("logp", 0), ("old_logp", 1), ("ref_logp", 2)):
+        want, ent, _ = O.forward_logprobs(pairs[k][1], O.BF16, V, V, B, T, lengths, tokens)
+        assert_close(outs[name].cpu().numpy().ravel()[m], want[m], what=f"{name} gap {gap}")
+        if k == 0:
+            assert_close(outs["entropy"].cpu().numpy().ravel()[m], ent[m], what=f"entropy gap {gap}")
+
+
+@pytest.mark.parametrize("P", [1, 2])
+def test_bf16_lazy_kernel_p1_p2(env, P):
+    """bf16 V = 152064 loss pass with one or two logits tensors (old / ref
+    log-probs precomputed): the lazy-running-max kernel (mix 7), against the
+    oracle, including rows that defeat a lazy max (the spike rows)."""
+    torch, rlo, obj = env
+    rng = np.random.default_rng(90 + P)
+    B, T, V = 2, 5, QWEN_V
+    lengths = np.array([5, 4], np.int32)
+    lg, host = synth_models(torch, rlo, B * T, V, seed=11)
+    spikes = spike_rows(V, SPIKES)  # the old rows of the first 4 tokens defeat a lazy max
+    old_rows = host[1].copy()
+    old_dev = lg[1].clone()
+    sd, sh = bf16_bits(torch, spikes)
+    old_dev[:len(SPIKES)] = sd
+    old_rows[:len(SPIKES)] = sh
+    tokens = rng.integers(0, V, (B, T)).astype(np.int32)
+    tokens.ravel()[:len(SPIKES)] = [sp[0][0] for sp in SPIKES]  # finite ratios on the spike rows
+    adv = rng.uniform(-1, 1, (B, T)).astype(np.float32)
+    ref_in = rng.uniform(-12, -2, (B, T)).astype(np.float32)
+    old_in = rng.uniform(-12, -2, (B, T)).astype(np.float32)
+    cfg = rlo.TrainConfig(kl_coef=0.001, kl_estimator="k3")
+    kw = dict(old_logits=old_dev) if P == 2 else dict(old_logprobs=dev(torch, old_in))
+    outs = obj.ppo_gradient(cfg, dev(torch, tokens), dev(torch, lengths), lg[0], dev(torch, adv),
+                            ref_logprobs=dev(torch, ref_in), outputs=("logp", "old_logp", "entropy", "loss"), **kw)
+    st = obj.merge_gradients(cfg)
+    m = valid_mask(B, T, lengths)
+    lp, ent, _ = O.forward_logprobs(host[0], O.BF16, V, V, B, T, lengths, tokens)
+    old = O.forward_logprobs(old_rows, O.BF16, V, V, B, T, lengths, tokens)[0] if P == 2 else \
+        old_in.astype(np.float64).ravel()
+    assert_close(outs["logp"].cpu().numpy().ravel()[m], lp[m], what="logp")
+    assert_close(outs["entropy"].cpu().numpy().ravel()[m], ent[m], what="entropy")
+    assert_close(outs["old_logp"].cpu().numpy().ravel()[m], old[m], what="old_logp")
+    oc = O.TrainConfig(kl_estimator=O.K3, kl_coef=0.001)
+    loss_tok, _, part = O.ppo_loss(oc, B, T, lengths, None, lp, old, ref_in.astype(np.float64).ravel(),
+                                   adv.astype(np.float64).ravel(), ent)
+    assert_close(outs["loss"].cpu().numpy().ravel(), loss_tok, tol=2e-5, what="loss_tok")
+    want = O.merge(part[None], oc)
+    for k in ("loss", "mean_ratio", "mean_kl", "mean_entropy"):
+        assert close(getattr(st, k), want[k]), (k, getattr(st, k), want[k])
 
 
 @pytest.mark.parametrize("pad", [8, 1, 16])
