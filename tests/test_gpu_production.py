@@ -339,7 +339,7 @@ def test_bf16_lockstep_offsets(env, off_old, off_ref, V):
 LS_FIRST = 3 * 256 * 8  # elements in the long-row lockstep kernel's first batch (U = 3 vectors x 256 threads)
 
 
-@pytest.mark.parametrize("gap", [0.0, 5.0, 10.0, 14.0, 40.0, "spike", "masked"])
+@pytest.mark.parametrize("gap", [0.0, 5.0, 10.0, 14.0, 40.0, "spike", "masked", "shift250", "shift300", "shift-400"])
 def test_bf16_long_lockstep_deferred_offset(env, gap):
     """The long-row lockstep kernel (bf16, V = 152064, P = 3) sums every batch
     after a thread's first against that first batch's actor max.  Rows whose
@@ -347,7 +347,9 @@ def test_bf16_long_lockstep_deferred_offset(env, gap):
     (s < 2^32) the entropy's log2 s - w/s cancels the gap's bits and must stay
     within 1e-5; above it (gap 40, one +60 spike) the share is redone exactly;
     "masked": a third of the actor row is -inf (masked vocabulary: guarded
-    redo).  Old / ref rows carry the same shape shifted by +-25 nats."""
+    redo); "shiftX": whole rows X nats off zero (the packed-bf16 clamp of the
+    polynomial lanes holds for offsets below 256 nats, larger ones keep the
+    fp32 clamp).  Old / ref rows carry the same shape shifted by +-25 nats."""
     torch, rlo, obj = env
     rng = np.random.default_rng(77 if isinstance(gap, str) else int(gap * 10))
     B, T, V = 2, 4, QWEN_V
@@ -357,6 +359,8 @@ def test_bf16_long_lockstep_deferred_offset(env, gap):
         rows[:, LS_FIRST + 8 * 1000 + 5] = 60.0
     elif gap == "masked":
         rows[:, rng.choice(V, V // 3, replace=False)] = -np.inf
+    elif isinstance(gap, str) and gap.startswith("shift"):
+        rows += float(gap[5:])
     else:
         rows[:, LS_FIRST:] += gap
     tensors = [rows, rows[::-1] + 25.0, rows + rng.standard_normal(rows.shape).astype(np.float32) * 0.2 - 25.0]
