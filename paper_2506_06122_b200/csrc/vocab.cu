@@ -30,11 +30,6 @@ constexpr int kWarps = kThreads / 32;
 #ifndef RLO_LDG_MIN_BLOCKS
 #define RLO_LDG_MIN_BLOCKS 4
 #endif
-// RLO_LS_BCLAMP = 1: the deferred lockstep batches clamp the polynomial lanes
-// on the packed bf16 words (HMNMX2) against bounds computed once per row.
-#ifndef RLO_LS_BCLAMP
-#define RLO_LS_BCLAMP 0
-#endif
 // RLO_ENT_GUARD_ALWAYS = 1: the entropy row always runs the guarded math
 // (no redo path).
 #ifndef RLO_ENT_GUARD_ALWAYS
@@ -62,12 +57,6 @@ __device__ __forceinline__ void lockstep_accumulate(const ET* const (&rows)[NT],
   const int tid = threadIdx.x;
   const int nvec = V / VT::kElems;
   const int nfull = nvec / kStep * kStep;
-  auto load = [&](int base, VV (&v)[NT][U]) {
-#pragma unroll
-    for (int k = 0; k < NT; ++k)
-#pragma unroll
-      for (int u = 0; u < U; ++u) v[k][u] = ld_stream(reinterpret_cast<const VV*>(rows[k]) + base + u * kThreads + tid);
-  };
   auto step = [&](const VV (&v)[NT][U]) {
     if (DEF && acc[0].mL > kLazyMin) {
       VT::template accumulate<U, true, MATH | kMathNoMax>(v[0], acc[0]);
@@ -89,40 +78,12 @@ __device__ __forceinline__ void lockstep_accumulate(const ET* const (&rows)[NT],
 #pragma unroll
     for (int k = 1; k < NT; ++k) VT::template accumulate<U, false, MATH | kMathNoMax>(v[k], acc[k]);
   };
-  int base = 0;
-  if constexpr (DEF && RLO_LS_BCLAMP && sizeof(ET) == 2 && poly_deg(MATH & kMathMask) > 0) {
-    // exact batches until the offset is set (normally just the first), then
-    // the deferred batches with the polynomial lanes clamped on the packed
-    // bf16 words against bounds computed once (offsets of |mL| >= kBcMax
-    // keep the per-element fp32 clamp in step())
-    for (; base < nfull;) {
-      VV v[NT][U];
-      load(base, v);
-      step(v);
-      base += kStep;
-      if (acc[0].mL > kLazyMin) break;
-    }
-    if (fabsf(acc[0].mL) < VT::kBcMax) {
-      uint32_t lo, hi;
-      VT::bc_bounds(acc[0].mL, lo, hi);
-      for (; base < nfull; base += kStep) {
-        VV v[NT][U];
-        load(base, v);
-        float cs, cw = 0.f;
-        VT::template sums<U, true, MATH | kMathNoMax>(v[0], acc[0].mL, cs, cw);
-        acc[0].s += cs;
-        acc[0].w += cw;
-#pragma unroll
-        for (int k = 1; k < NT; ++k) {
-          VT::template sums_bc<U, MATH>(v[k], acc[k].mL, lo, hi, cs);
-          acc[k].s += cs;
-        }
-      }
-    }
-  }
-  for (; base < nfull; base += kStep) {
+  for (int base = 0; base < nfull; base += kStep) {
     VV v[NT][U];
-    load(base, v);
+#pragma unroll
+    for (int k = 0; k < NT; ++k)
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[k][u] = ld_stream(reinterpret_cast<const VV*>(rows[k]) + base + u * kThreads + tid);
     step(v);
   }
   if (nfull < nvec) {

@@ -160,15 +160,12 @@ constexpr float kLazyMin = -1.0e29f;      // mL above this holds a real max (ini
 // Two FMNMX per element pair, so the entropy row runs unguarded and a thread
 // whose entropy sum comes out non-finite redoes its share guarded (vocab.cu,
 // fused.cu); the batch padding is finite (fill()) and never triggers it.
-// PRE: the caller already clamped the polynomial lanes' logits on the packed
-// bf16 word (Vec<bf16>::sums_bc), so t is inside the domain.
-template <bool ENT, bool GUARD, bool PRE = false>
+template <bool ENT, bool GUARD>
 __device__ __forceinline__ void pair2(float zl, float zh, f2 L2, f2 nmL, f2& s, f2& w, int poly) {
   const f2 t = ffma2(pk2(zl, zh), L2, nmL);
   float tl, th;
   upk2(t, tl, th);
-  if (poly && PRE) {
-  } else if (poly) {
+  if (poly) {
     // the polynomial's domain: 2^j is inserted into the exponent field, so j
     // must stay in [-126, 127].  The upper clamp matters under the lazy max
     // and lockstep streams, where t can be positive: an element far above the
@@ -330,43 +327,6 @@ struct Vec<__nv_bfloat16> {
   template <int U, bool ENT, int MATHG>
   __device__ static void accumulate(const V (&v)[U], Acc& a) {
     accumulate_chunk<Vec<__nv_bfloat16>, U, ENT, MATHG>(v, a);
-  }
-  // Polynomial-lane clamp on the packed bf16 word (one HMNMX2 per bound and
-  // word instead of two FMNMX per element): bounds for an offset mL whose
-  // |mL| < kBcMax, so that the bf16 spacing near the bounds (<= 2) keeps a
-  // clamped element's term at <= 2^-122 and the upper bound's at >= 2^123
-  // (the range checks redo the share).  lo / hi: bf16x2 of the smallest logit
-  // with t >= -125 and the largest with t <= 126.
-  static constexpr float kBcMax = 256.0f * kL2E;
-  __device__ static void bc_bounds(float mL, uint32_t& lo, uint32_t& hi) {
-    const float inv = 1.0f / kL2E;
-    const __nv_bfloat16 l = __float2bfloat16_ru((mL - 125.0f) * inv), h = __float2bfloat16_rd((mL + 126.0f) * inv);
-    const __nv_bfloat162 l2 = __halves2bfloat162(l, l), h2 = __halves2bfloat162(h, h);
-    lo = *reinterpret_cast<const uint32_t*>(&l2);
-    hi = *reinterpret_cast<const uint32_t*>(&h2);
-  }
-  __device__ static uint32_t bc_clamp(uint32_t x, uint32_t lo, uint32_t hi) {
-    const __nv_bfloat162 r = __hmin2(__hmax2(as_b2(x), as_b2(lo)), as_b2(hi));
-    return *reinterpret_cast<const uint32_t*>(&r);
-  }
-  // sums() of a no-entropy row with the polynomial lanes clamped by bc_clamp
-  // (MATH without kMathGuard; quarter or half offload as vec_sums).
-  template <int U, int MATHG>
-  __device__ static void sums_bc(const V (&v)[U], float mL, uint32_t lo, uint32_t hi, float& cs) {
-    constexpr int MATH = MATHG & kMathMask;
-    const f2 L2 = pk2(kL2E, kL2E), nmL = pk2(-mL, -mL);
-    f2 s0 = 0, s1 = 0, w0 = 0, w1 = 0;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int py = (poly_odd_only(MATH) && !(u & 1)) ? 0 : poly_deg(MATH);
-      const uint32_t y = py ? bc_clamp(v[u].y, lo, hi) : v[u].y;
-      const uint32_t ww = poly_half(MATH) ? bc_clamp(v[u].w, lo, hi) : v[u].w;
-      pair2<false, false>(bf16lo(v[u].x), bf16hi(v[u].x), L2, nmL, s0, w0, 0);
-      pair2<false, false, true>(bf16lo(y), bf16hi(y), L2, nmL, s1, w1, py);
-      pair2<false, false>(bf16lo(v[u].z), bf16hi(v[u].z), L2, nmL, s0, w0, 0);
-      pair2<false, false, true>(bf16lo(ww), bf16hi(ww), L2, nmL, s1, w1, poly_half(MATH) ? poly_deg(MATH) : 0);
-    }
-    cs = hsum2(s0, s1);
   }
   __device__ static float scalar(const __nv_bfloat16* p) {
     return __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(p)));
