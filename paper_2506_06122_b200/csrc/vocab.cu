@@ -49,6 +49,10 @@ constexpr int kWarps = kThreads / 32;
 // actor max of the thread's first batch only; later batches take no max, test
 // or rescale at all -- the kernel's range checks on the finished shares redo
 // any share that left the safe range.
+// Thread tid's share is the vectors base + u * kThreads + tid -- the layout of
+// stream_accumulate with the same U, so a redo covers exactly the share it
+// replaces (a 256-bit pair layout here would break that; it also read 0.6%
+// fewer bytes, profiles/r2_vocab_ab.txt call t).
 template <typename ET, int NT, int U, int MATH, bool DEF = false>
 __device__ __forceinline__ void lockstep_accumulate(const ET* const (&rows)[NT], int V, Acc (&acc)[NT]) {
   using VT = Vec<ET>;
