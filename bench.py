@@ -589,6 +589,9 @@ def main():
         os.close(real_stdout)
     if out is not None:
         print(json.dumps(out), flush=True)
+    # exit-time library output (NCCL's plugin teardown prints INFO lines at
+    # process exit under NCCL_DEBUG=INFO) goes to stderr, after the one line
+    os.dup2(2, 1)
 
 
 if __name__ == "__main__":
