@@ -1,2 +1,2 @@
-RLO_LIB=$PWD/paper_2506_06122_b200/lib/variants/librlo_bc.so timeout 900 python -m pytest tests/test_gpu_production.py tests/test_gpu_guards.py tests/test_gpu_parity.py tests/test_gpu_edges.py -m gpu -q -p no:cacheprovider 2>&1 | tail -2
-bash tools/ab_bench.sh s 3 cur bc bcb3 | tee gpurun_out/r2s_ab.txt
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider -rf 2>&1 | tail -8
+bash tools/ab_bench.sh w 2 cur new | tee gpurun_out/r2w_ab.txt

@@ -111,6 +111,21 @@ __device__ __forceinline__ f2 exp2_poly2(float tl, float th) {
   return pk2(__uint_as_float(bl), __uint_as_float(bh));
 }
 
+// max / min that return NaN when either input is NaN (FMNMX.NAN, same cost as
+// fmaxf / fminf, which return the other operand): a clamp of an exponent
+// argument must not turn a NaN logit into a finite term -- the reference's
+// log-sum-exp of a row holding a NaN is NaN (policy.cpp:117-121).
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
 __device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 

@@ -233,7 +233,8 @@ cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
 //        lockstep, U = 3 per tensor, on a deferred offset (the actor max of
 //        the thread's first batch; no per-batch max, test or rescale):
 //        +3-4% over the per-tensor lazy-max streams at the power cap
-//        (profiles/r2_vocab_ab.txt).
+//        (profiles/r2_vocab_ab.txt); the 2-tensor loss pass (actor + old or
+//        ref) over long rows the same way (+3%).
 #ifndef RLO_F32_MATH
 #define RLO_F32_MATH 1
 #endif
@@ -258,6 +259,9 @@ cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
 #ifndef RLO_BF16_LONG_LS
 #define RLO_BF16_LONG_LS 3
 #endif
+#ifndef RLO_BF16_LS_P2
+#define RLO_BF16_LS_P2 1
+#endif
 #ifndef RLO_BF16_LONG_LS_MATH
 #define RLO_BF16_LONG_LS_MATH RLO_BF16_SHORT_MATH
 #endif
@@ -275,6 +279,12 @@ cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
     if constexpr (NT == 3 && LOSS && RLO_BF16_LONG_LS != 0) {  // lockstep: short rows / long rows
       if (a.V < kLongRowV) return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_SHORT_MATH, 2, false, true>(a, num_sms, s);
       return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_LONG_LS_MATH | kMathDeferred, RLO_BF16_LONG_LS, false, true>(
+          a, num_sms, s);
+    } else if constexpr (NT == 2 && LOSS && RLO_BF16_LONG_LS != 0 && RLO_BF16_LS_P2) {  // P = 2: long rows lockstep
+      if (a.V >= kLongRowV)
+        return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_LONG_LS_MATH | kMathDeferred, RLO_BF16_LONG_LS, false, true>(
+            a, num_sms, s);
+      return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, false, RLO_BF16_UN, RLO_BF16_PFN>(
           a, num_sms, s);
     } else {
       if constexpr (NT == 3 && LOSS)

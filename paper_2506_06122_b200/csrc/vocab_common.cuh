@@ -172,11 +172,12 @@ __device__ __forceinline__ void pair2(float zl, float zh, f2 L2, f2 nmL, f2& s, 
     // running max then yields 2^127 (the chunk sum fails the lazy cap / the
     // lockstep range check and is redone the exact way) instead of a wrapped
     // exponent that would silently drop the dominant term.
-    tl = fminf(fmaxf(tl, -126.0f), 127.0f);
-    th = fminf(fmaxf(th, -126.0f), 127.0f);
+    // (NaN-propagating clamps: a NaN logit keeps the share NaN, as in the reference)
+    tl = fmin_nan(fmax_nan(tl, -126.0f), 127.0f);
+    th = fmin_nan(fmax_nan(th, -126.0f), 127.0f);
   } else if (ENT && GUARD) {
-    tl = fmaxf(tl, -126.0f);
-    th = fmaxf(th, -126.0f);
+    tl = fmax_nan(tl, -126.0f);
+    th = fmax_nan(th, -126.0f);
   }
   const f2 e = poly == 5 ? exp2_poly2<5>(tl, th) : poly == 4 ? exp2_poly2<4>(tl, th) : pk2(ex2(tl), ex2(th));
   s = fadd2(s, e);
@@ -209,6 +210,15 @@ __device__ __forceinline__ void accumulate_chunk(const typename VT::V (&v)[U], A
   }
   if (!(MATHG & kMathNoMax)) acc_rescale<ENT>(a, VT::template chunk_max<U>(v));
   VT::template sums<U, ENT, MATHG>(v, a.mL, cs, cw);
+  constexpr int kM = MATHG & kMathMask;
+  if constexpr ((MATHG & kMathNoMax) == 0 && (ENT ? poly_deg_ent(kM) : poly_deg(kM)) > 0) {
+    // Against the chunk's own max every term is <= 1, so a sum >= 2^100 can
+    // only come from a NaN logit in a polynomial lane: the exponent insertion
+    // of exp2_poly2 turns the NaN into FLT_MAX.  Keep it NaN, as MUFU lanes
+    // and the reference do (the lazy / lockstep checks above route such
+    // chunks and shares here).
+    if (!(cs < 0x1p100f)) cs = __int_as_float(0x7fffffff);
+  }
   a.s += cs;
   if (ENT) a.w += cw;
 }

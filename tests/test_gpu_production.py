@@ -14,7 +14,8 @@ rlo_objective_step_host_mb):
   rows that defeat a lazy max / deferred offset: every element far below one
   spike that sits in a polynomial lane (the .y word of a uint4), actor rows
   whose later batches sit 5-40 nats above the first, -inf masked entries;
-* bf16 V = 152064, P = 1 / 2: the lazy-running-max kernel (mix 7);
+* bf16 P = 2 over long rows: the same lockstep kernel with two tensors;
+* bf16 P = 1, and P = 2 over short rows: the lazy-running-max kernel (mix 7);
 * bf16 V < 65536, P = 3: the short-row lockstep kernel (old/ref sums on the
   actor's running max); both lockstep kernels with old/ref rows far above and
   far below the actor's;
@@ -384,24 +385,27 @@ def test_bf16_long_lockstep_deferred_offset(env, gap):
             assert_close(outs["entropy"].cpu().numpy().ravel()[m], ent[m], what=f"entropy gap {gap}")
 
 
+@pytest.mark.parametrize("V", [QWEN_V, 32000])
 @pytest.mark.parametrize("P", [1, 2])
-def test_bf16_lazy_kernel_p1_p2(env, P):
-    """bf16 V = 152064 loss pass with one or two logits tensors (old / ref
-    log-probs precomputed): the lazy-running-max kernel (mix 7), against the
-    oracle, including rows that defeat a lazy max (the spike rows)."""
+def test_bf16_p1_p2_kernels(env, P, V):
+    """bf16 loss pass with one or two logits tensors (old / ref log-probs
+    precomputed) against the oracle: P = 1 (any V) and P = 2 short rows take
+    the lazy-running-max kernel (mix 7), P = 2 long rows the lockstep kernel
+    on a deferred offset; at V = 152064 the old rows of the first tokens are
+    the spike rows that defeat a lazy max."""
     torch, rlo, obj = env
     rng = np.random.default_rng(90 + P)
-    B, T, V = 2, 5, QWEN_V
+    B, T = 2, 5
     lengths = np.array([5, 4], np.int32)
     lg, host = synth_models(torch, rlo, B * T, V, seed=11)
-    spikes = spike_rows(V, SPIKES)  # the old rows of the first 4 tokens defeat a lazy max
     old_rows = host[1].copy()
     old_dev = lg[1].clone()
-    sd, sh = bf16_bits(torch, spikes)
-    old_dev[:len(SPIKES)] = sd
-    old_rows[:len(SPIKES)] = sh
     tokens = rng.integers(0, V, (B, T)).astype(np.int32)
-    tokens.ravel()[:len(SPIKES)] = [sp[0][0] for sp in SPIKES]  # finite ratios on the spike rows
+    if V == QWEN_V:
+        sd, sh = bf16_bits(torch, spike_rows(V, SPIKES))
+        old_dev[:len(SPIKES)] = sd
+        old_rows[:len(SPIKES)] = sh
+        tokens.ravel()[:len(SPIKES)] = [sp[0][0] for sp in SPIKES]  # finite ratios on the spike rows
     adv = rng.uniform(-1, 1, (B, T)).astype(np.float32)
     ref_in = rng.uniform(-12, -2, (B, T)).astype(np.float32)
     old_in = rng.uniform(-12, -2, (B, T)).astype(np.float32)
@@ -463,6 +467,41 @@ def test_bf16_row_alignments(env, pad):
 
 
 # ---- every shipped forward_logprobs instantiation --------------------------------------------------
+
+@pytest.mark.parametrize("V,stride", [(100003, 100008), (70001, 70001), (65536, 65536), (65535, 65544)])
+def test_bf16_long_rows_odd_vocab(env, V, stride):
+    """Long bf16 rows (>= 64 Ki elements take the long-row lockstep kernel)
+    with a vocabulary that is not a multiple of the 16-byte vector: aligned
+    rows (stride a multiple of 8) run the lockstep batches, the partial batch
+    and the scalar tail; a contiguous odd vocabulary misaligns every other row
+    (per-tensor fallback inside the same kernel); V = 65536 / 65535 sit at the
+    short/long boundary.  P = 3 loss pass against the oracle."""
+    torch, rlo, obj = env
+    rng = np.random.default_rng(V)
+    B, T = 2, 3
+    lengths = np.array([3, 2], np.int32)
+    dev_rows, host_rows = [], []
+    for k in range(3):
+        r = rng.standard_normal((B * T, V)).astype(np.float32) * 2.5 + (0.0, 9.0, -9.0)[k]
+        full = torch.zeros(B * T, stride, dtype=torch.bfloat16)
+        full[:, :V] = torch.from_numpy(r).to(torch.bfloat16)
+        dev_rows.append(full.cuda()[:, :V])
+        host_rows.append(full[:, :V].contiguous().view(torch.int16).numpy().view(np.uint16))
+    tokens = rng.integers(0, V, (B, T)).astype(np.int32)
+    tokens[0, 0] = V - 1  # the scalar tail's last element
+    cfg = rlo.TrainConfig(kl_coef=0.01, kl_estimator="k3")
+    outs = obj.ppo_gradient(cfg, dev(torch, tokens), dev(torch, lengths), dev_rows[0],
+                            dev(torch, rng.uniform(-1, 1, (B, T)).astype(np.float32)),
+                            old_logits=dev_rows[1], ref_logits=dev_rows[2],
+                            outputs=("logp", "old_logp", "ref_logp", "entropy"))
+    obj.merge_gradients(cfg)
+    m = valid_mask(B, T, lengths)
+    for name, k in (("logp", 0), ("old_logp", 1), ("ref_logp", 2)):
+        want, ent, _ = O.forward_logprobs(host_rows[k], O.BF16, V, V, B, T, lengths, tokens)
+        assert_close(outs[name].cpu().numpy().ravel()[m], want[m], what=f"{name} V {V} stride {stride}")
+        if k == 0:
+            assert_close(outs["entropy"].cpu().numpy().ravel()[m], ent[m], what="entropy")
+
 
 @pytest.mark.parametrize("dt,V", [("f32", 32000), ("bf16", QWEN_V), ("bf16", 4096)])
 @pytest.mark.parametrize("entropy", [False, True])
@@ -597,3 +636,52 @@ def test_decode_tiny_temperature(env, temp, scale):
         assert tok[i] == want, (i, tok[i], want)
         assert tok[i] == int(np.argmax(rows[i]))  # greedy at this temperature (no exact ties here)
         assert abs(lp[i] - want_lp) <= 1e-5 * max(1.0, abs(want_lp))
+
+
+# ---- NaN logits propagate (policy.cpp:117-121: the log-sum-exp of a row holding a NaN is NaN) ------
+
+@pytest.mark.parametrize("dt,V", [("bf16", QWEN_V), ("bf16", 32000), ("f32", 32000)])
+def test_nan_logit_propagates_loss_pass(env, dt, V):
+    """A NaN in one row of each tensor -- in a MUFU lane (actor) and in the
+    polynomial lanes (.y word, old / ref) past the first batch -- makes that
+    token's log-prob NaN (no clamp turns it into a finite term, no redo hides
+    it); the other tokens stay finite and the merge refuses the step like the
+    reference (TrainingError, policy.cpp:441-448)."""
+    torch, rlo, obj = env
+    rng = np.random.default_rng(5)
+    B, T = 1, 4
+    lengths = np.array([4], np.int32)
+    rows = [rng.standard_normal((B * T, V)).astype(np.float32) * 2 for _ in range(3)]
+    rows[0][0, 8200] = np.nan   # actor, row 0
+    rows[1][1, 8194] = np.nan   # old, row 1 (polynomial lane)
+    rows[2][2, 20003] = np.nan  # ref, row 2 (polynomial lane)
+    if dt == "bf16":
+        x = [bf16_bits(torch, r)[0] for r in rows]
+    else:
+        x = [dev(torch, r) for r in rows]
+    tokens = rng.integers(0, V, (B, T)).astype(np.int32)
+    cfg = rlo.TrainConfig(kl_coef=0.01, kl_estimator="k3")
+    outs = obj.ppo_gradient(cfg, dev(torch, tokens), dev(torch, lengths), x[0], dev(torch, np.zeros((B, T), np.float32)),
+                            old_logits=x[1], ref_logits=x[2], outputs=("logp", "old_logp", "ref_logp", "entropy"))
+    with pytest.raises(rlo.TrainingError):
+        obj.merge_gradients(cfg)
+    lp, old, ref = (outs[k].cpu().numpy().ravel() for k in ("logp", "old_logp", "ref_logp"))
+    assert np.isnan(lp[0]) and np.isnan(outs["entropy"].cpu().numpy().ravel()[0])
+    assert np.isnan(old[1]) and np.isnan(ref[2])
+    assert np.isfinite(lp[1:]).all() and np.isfinite(old[[0, 2, 3]]).all() and np.isfinite(ref[[0, 1, 3]]).all()
+
+
+@pytest.mark.parametrize("dt,V", [("bf16", QWEN_V), ("f32", 32000)])
+@pytest.mark.parametrize("entropy", [False, True])
+def test_nan_logit_propagates_forward_logprobs(env, dt, V, entropy):
+    torch, rlo, obj = env
+    rng = np.random.default_rng(6)
+    rows = rng.standard_normal((3, V)).astype(np.float32) * 2
+    rows[1, 8194] = np.nan  # polynomial lane of the no-entropy bf16 mix
+    x = bf16_bits(torch, rows)[0] if dt == "bf16" else dev(torch, rows)
+    out = obj.forward_logprobs(x, dev(torch, np.array([[5, 6, 7]], np.int32)), dev(torch, np.array([3], np.int32)),
+                               entropy=entropy)
+    lp = out["logp"].cpu().numpy().ravel()
+    assert np.isnan(lp[1]) and np.isfinite(lp[[0, 2]]).all()
+    if entropy:
+        assert np.isnan(out["entropy"].cpu().numpy().ravel()[1])
