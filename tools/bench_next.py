@@ -7,6 +7,8 @@
              SampleBatch::from_jsonl + validate (oracle/_ref, when built): MB/s of JSONL
   broadcast  ModelUpdateGroup bucketed NCCL broadcast (rlo_broadcast_params), under torchrun
              with >= 2 ranks: algorithm bandwidth per bucket size
+  reference  the reference's own CPU code for decode / actor backward / value / advantages
+             (oracle/_ref, cpu_baseline role) on all host threads, bounded samples
 
 The actor backward epilogue (row 1) is measured by tools/bench_update.py.
 
@@ -141,6 +143,60 @@ def bench_jsonl():
         print(json.dumps(out), flush=True)
 
 
+def bench_reference():
+    """The reference's own CPU code for the same rows (oracle/_ref, the
+    cpu_baseline role: timed beside the GPU numbers, never the product), on
+    all host threads over a bounded sample: ctypes drops the GIL inside each
+    call, so one Python thread per core runs the reference's functions in
+    parallel like the reference's thread-per-rank cluster."""
+    import concurrent.futures as cf
+
+    import oracle as O
+    if not O.ref_available():
+        print(json.dumps({"row": "reference", "unavailable": "oracle/_ref not built"}), flush=True)
+        return
+    nt = os.cpu_count() or 1
+    pool = cf.ThreadPoolExecutor(nt)
+
+    def par(fn, n):
+        t0 = time.perf_counter()
+        list(pool.map(fn, range(n)))
+        return time.perf_counter() - t0
+
+    V = 152064
+    rng = np.random.default_rng(3)
+    rows = [rng.standard_normal(V) * 3.0 for _ in range(nt)]
+    for temp in (0.8, 1.0):  # decode_next (policy.cpp:143-169) on one logits row each
+        n = 4 * nt
+        s = par(lambda i: O.ref_decode_b2(rows[i % nt], temp, 42, 3, 7919 * i, 17), n)
+        print(json.dumps({"row": "decode", "impl": "reference", "V": V, "temperature": temp, "rows": n,
+                          "threads": nt, "s": s, "rows_per_s": n / s}), flush=True)
+    T = 8  # ppo_gradient incl. its actor backward dz = dlp (onehot - p) (policy.cpp:313-379), b2 trick
+    lengths, mask = np.array([T], np.int32), np.ones(T, np.uint8)
+    toks = rng.integers(0, V, T).astype(np.int32)
+    lp = np.full(T, -3.0)
+    adv = rng.uniform(-1, 1, T)
+    cfg = O.TrainConfig(kl_coef=0.001)
+    n = 2 * nt
+    s = par(lambda i: O.ref_ppo_grad_b2(rows[i % nt], 1, T, lengths, toks, mask, lp, lp, adv, cfg), n)
+    print(json.dumps({"row": "backward", "impl": "reference", "V": V, "tokens": n * T, "threads": nt, "s": s,
+                      "tokens_per_s": n * T / s, "note": "ppo_gradient: log-softmax + loss + dz per token"}),
+          flush=True)
+    B, T = 256, 16384  # value_gradient (policy.cpp:474-540) and compute_advantages (policy.cpp:257-311)
+    L = np.full(B, T, np.int32)
+    tg = rng.standard_normal(B * T)
+    s = par(lambda i: O.ref_value_loss_b2(0.1, B // nt or 1, T, L[:B // nt or 1], None, tg[:(B // nt or 1) * T]), nt)
+    print(json.dumps({"row": "value", "impl": "reference", "B": B, "T": T, "threads": nt, "s": s,
+                      "tokens_per_s": (B // nt or 1) * nt * T / s}), flush=True)
+    acfg = O.TrainConfig(whiten_advantages=1, gamma=0.99)
+    bt = B // nt or 1
+    s = par(lambda i: O.ref_compute_advantages(acfg, bt, T, L[:bt], None, rewards_seq=np.ones(bt)), nt)
+    print(json.dumps({"row": "advantages", "impl": "reference", "estimator": "reinforce", "B": B, "T": T,
+                      "threads": nt, "s": s, "tokens_per_s": bt * nt * T / s,
+                      "note": "per-thread shards whitened locally (the reference has no GRPO/GAE)"}), flush=True)
+    pool.shutdown()
+
+
 def bench_broadcast():
     import torch.distributed as dist
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -167,7 +223,7 @@ def bench_broadcast():
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="decode,value,advantages,jsonl")
+    ap.add_argument("--only", default="decode,value,advantages,jsonl,reference")
     args = ap.parse_args()
     rows = args.only.split(",")
     if "broadcast" in rows:
@@ -182,6 +238,8 @@ def main():
         bench_advantages(obj)
     if "jsonl" in rows:
         bench_jsonl()
+    if "reference" in rows:
+        bench_reference()
 
 
 if __name__ == "__main__":
