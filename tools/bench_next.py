@@ -158,17 +158,19 @@ def bench_reference():
     nt = os.cpu_count() or 1
     pool = cf.ThreadPoolExecutor(nt)
 
-    def par(fn, n):
-        t0 = time.perf_counter()
-        list(pool.map(fn, range(n)))
-        return time.perf_counter() - t0
+    def par(fn, n, budget=1.5):
+        """Rounds of n calls over the pool until `budget` seconds: (s, calls)."""
+        t0, k = time.perf_counter(), 0
+        while k == 0 or time.perf_counter() - t0 < budget:
+            list(pool.map(fn, range(k * n, (k + 1) * n)))
+            k += 1
+        return time.perf_counter() - t0, k * n
 
     V = 152064
     rng = np.random.default_rng(3)
     rows = [rng.standard_normal(V) * 3.0 for _ in range(nt)]
     for temp in (0.8, 1.0):  # decode_next (policy.cpp:143-169) on one logits row each
-        n = 4 * nt
-        s = par(lambda i: O.ref_decode_b2(rows[i % nt], temp, 42, 3, 7919 * i, 17), n)
+        s, n = par(lambda i: O.ref_decode_b2(rows[i % nt], temp, 42, 3, 7919 * i, 17), nt)
         print(json.dumps({"row": "decode", "impl": "reference", "V": V, "temperature": temp, "rows": n,
                           "threads": nt, "s": s, "rows_per_s": n / s}), flush=True)
     T = 8  # ppo_gradient incl. its actor backward dz = dlp (onehot - p) (policy.cpp:313-379), b2 trick
@@ -177,22 +179,21 @@ def bench_reference():
     lp = np.full(T, -3.0)
     adv = rng.uniform(-1, 1, T)
     cfg = O.TrainConfig(kl_coef=0.001)
-    n = 2 * nt
-    s = par(lambda i: O.ref_ppo_grad_b2(rows[i % nt], 1, T, lengths, toks, mask, lp, lp, adv, cfg), n)
+    s, n = par(lambda i: O.ref_ppo_grad_b2(rows[i % nt], 1, T, lengths, toks, mask, lp, lp, adv, cfg), nt)
     print(json.dumps({"row": "backward", "impl": "reference", "V": V, "tokens": n * T, "threads": nt, "s": s,
                       "tokens_per_s": n * T / s, "note": "ppo_gradient: log-softmax + loss + dz per token"}),
           flush=True)
     B, T = 256, 16384  # value_gradient (policy.cpp:474-540) and compute_advantages (policy.cpp:257-311)
     L = np.full(B, T, np.int32)
     tg = rng.standard_normal(B * T)
-    s = par(lambda i: O.ref_value_loss_b2(0.1, B // nt or 1, T, L[:B // nt or 1], None, tg[:(B // nt or 1) * T]), nt)
-    print(json.dumps({"row": "value", "impl": "reference", "B": B, "T": T, "threads": nt, "s": s,
-                      "tokens_per_s": (B // nt or 1) * nt * T / s}), flush=True)
-    acfg = O.TrainConfig(whiten_advantages=1, gamma=0.99)
     bt = B // nt or 1
-    s = par(lambda i: O.ref_compute_advantages(acfg, bt, T, L[:bt], None, rewards_seq=np.ones(bt)), nt)
+    s, n = par(lambda i: O.ref_value_loss_b2(0.1, bt, T, L[:bt], None, tg[:bt * T]), nt)
+    print(json.dumps({"row": "value", "impl": "reference", "B": B, "T": T, "threads": nt, "s": s,
+                      "tokens_per_s": bt * n * T / s}), flush=True)
+    acfg = O.TrainConfig(whiten_advantages=1, gamma=0.99)
+    s, n = par(lambda i: O.ref_compute_advantages(acfg, bt, T, L[:bt], None, rewards_seq=np.ones(bt)), nt)
     print(json.dumps({"row": "advantages", "impl": "reference", "estimator": "reinforce", "B": B, "T": T,
-                      "threads": nt, "s": s, "tokens_per_s": bt * nt * T / s,
+                      "threads": nt, "s": s, "tokens_per_s": bt * n * T / s,
                       "note": "per-thread shards whitened locally (the reference has no GRPO/GAE)"}), flush=True)
     pool.shutdown()
 
