@@ -30,9 +30,6 @@ constexpr int kWarps = kThreads / 32;
 #ifndef RLO_LDG_MIN_BLOCKS
 #define RLO_LDG_MIN_BLOCKS 4
 #endif
-#ifndef RLO_TOK_PREFETCH
-#define RLO_TOK_PREFETCH 0
-#endif
 // RLO_ENT_GUARD_ALWAYS = 1: the entropy row always runs the guarded math
 // (no redo path).
 #ifndef RLO_ENT_GUARD_ALWAYS
@@ -123,13 +120,7 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t nrows = (int64_t)a.B * a.T;
   int buf = 0;
-  // RLO_TOK_PREFETCH: thread 0 loads the token id of the CTA's next row while
-  // this one streams, so the gather's dependent load chain (token id, then the
-  // logits at it) never stalls warp 0 at a row start.
-  int tok_next = (RLO_TOK_PREFETCH && tid == 0 && blockIdx.x < nrows) ? __ldg(a.tokens + blockIdx.x) : 0;
   for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
-    const int tok_row = tok_next;
-    if (RLO_TOK_PREFETCH && tid == 0 && row + gridDim.x < nrows) tok_next = __ldg(a.tokens + row + gridDim.x);
     if (!row_active<LOSS>(a, row, tid == 0)) {  // uniform across the CTA
       if (tid == 0) write_inactive<LOSS>(a, row);
       continue;
@@ -137,12 +128,7 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
     int tok = 0;
     bool oov = false;
     float ztok[NT];
-    if (tid == 0) {
-      if (RLO_TOK_PREFETCH)
-        gather_token_id<ET, NT>(a, row, tok_row, tok, oov, ztok);
-      else
-        gather_token<ET, NT>(a, row, tok, oov, ztok);
-    }
+    if (tid == 0) gather_token<ET, NT>(a, row, tok, oov, ztok);
     Acc acc[NT];
     if constexpr (LS && NT >= 2 && ENT0) {
       const ET* rows[NT];

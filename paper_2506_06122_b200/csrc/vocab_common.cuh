@@ -683,18 +683,7 @@ __device__ __forceinline__ bool row_exists(const VocabArgs& a, int64_t row) {
   return row - (int64_t)b * a.T < seq_len(a.lengths, b, a.T);
 }
 
-// Token gather for the row (one thread): bit-exact element loads.  The
-// overload with `known` takes the token id already loaded (prefetched one row
-// ahead by the caller), so only the logit loads remain and nothing waits on
-// the token id's latency.
-template <typename ET, int NT>
-__device__ __forceinline__ void gather_token_id(const VocabArgs& a, int64_t row, int tok_in, int& tok, bool& oov,
-                                                float (&ztok)[NT]) {
-  tok = tok_in;
-  oov = tok < 0 || tok >= a.V;
-#pragma unroll
-  for (int k = 0; k < NT; ++k) ztok[k] = oov ? 0.f : load_logit<ET>(a.logits[k], logits_off(a, k, row) + tok);
-}
+// Token gather for the row (one thread): bit-exact element loads.
 template <typename ET, int NT>
 __device__ __forceinline__ void gather_token(const VocabArgs& a, int64_t row, int& tok, bool& oov, float (&ztok)[NT]) {
   tok = __ldg(a.tokens + row);
