@@ -271,20 +271,25 @@ __device__ __forceinline__ float raw_max(const uint4 (&r)[U]) {
 // the untempered sum at T != 1, which only feeds the returned log-prob
 // (|lse error| <= 1.5e-6), so the MUFU pipe carries 1.5 instead of 2
 // exponentials per element there.  Never used for the certified weights.
+// Returns the fp32 vector sum: the caller adds the U vectors of a batch in
+// fp32 and converts once (this sum needs ~1e-6, not the certificate's bound).
 template <typename ET>
-__device__ __forceinline__ double vec_wsum_half_poly(const uint4& r, float c, float mo) {
+__device__ __forceinline__ float vec_wsum_half_poly(const uint4& r, float c, float mo) {
   constexpr int E = RawVec<ET>::E;
+  const f2 c2 = pk2(c, c), m2 = pk2(-mo, -mo);
   f2 acc = pk2(0.f, 0.f);
 #pragma unroll
   for (int p = 0; p < E / 2; ++p) {
-    const float tl = fmaf(RawVec<ET>::at(r, 2 * p), c, -mo), th = fmaf(RawVec<ET>::at(r, 2 * p + 1), c, -mo);
+    const f2 t = ffma2(pk2(RawVec<ET>::at(r, 2 * p), RawVec<ET>::at(r, 2 * p + 1)), c2, m2);  // = two fmaf
+    float tl, th;
+    upk2(t, tl, th);
     const bool poly = RLO_SCREEN_POLY == 2 ? true : RLO_SCREEN_POLY == 1 ? (p & 1) != 0 : false;
     const f2 e = poly ? exp2_poly2<4>(fmaxf(tl, -126.f), fmaxf(th, -126.f)) : pk2(ex2(tl), ex2(th));
     acc = fadd2(acc, e);
   }
   float lo, hi;
   upk2(acc, lo, hi);
-  return (double)(lo + hi);
+  return lo + hi;
 }
 
 // The screened fp32 path for one row (every thread of the CTA calls it; the
@@ -314,10 +319,16 @@ __device__ __forceinline__ bool screened_row(const ET* __restrict__ z, int V, in
   const int v0 = warp * W, v1 = min(V, v0 + W);
   float m = -INFINITY, mL = kNegInit * kL2E, mT = kNegInit * kL2E;
   double st = 0.0, su = 0.0;
-  for (int b = v0 + lane * E; b < v1; b += U * S) {
-    uint4 r[U];
+  auto load = [&](int b, uint4 (&r)[U]) {
+    if (vec_ok && b + (U - 1) * S + E <= v1) {  // whole batch in range: plain vector loads
 #pragma unroll
-    for (int k = 0; k < U; ++k) r[k] = load_raw<ET>(z, b + k * S, v1, vec_ok);
+      for (int k = 0; k < U; ++k) r[k] = ld_stream(reinterpret_cast<const uint4*>(z + b + k * S));
+    } else {
+#pragma unroll
+      for (int k = 0; k < U; ++k) r[k] = load_raw<ET>(z, b + k * S, v1, vec_ok);
+    }
+  };
+  auto batch = [&](const uint4 (&r)[U]) {
     const float cm = raw_max<ET, U>(r);
     if (cm > m) {
       const float nL = __fmul_rn(cm, kL2E), nT = unit_t ? nL : __fmul_rn(cm, cT);
@@ -325,7 +336,7 @@ __device__ __forceinline__ bool screened_row(const ET* __restrict__ z, int V, in
       st *= exp2((double)mT - (double)nT);
       m = cm, mL = nL, mT = nT;
     }
-    if (m == -INFINITY) continue;
+    if (m == -INFINITY) return;
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       if (unit_t) {  // one set of weights, certified precision
@@ -333,10 +344,20 @@ __device__ __forceinline__ bool screened_row(const ET* __restrict__ z, int V, in
         su += qs;
         st += qs;
       } else {
-        su += vec_wsum_half_poly<ET>(r[k], kL2E, mL);
         st += vec_wsum<ET>(r[k], cT, mT);
       }
     }
+    if (!unit_t) {
+      float sb = 0.f;
+#pragma unroll
+      for (int k = 0; k < U; ++k) sb += vec_wsum_half_poly<ET>(r[k], kL2E, mL);
+      su += (double)sb;
+    }
+  };
+  for (int b = v0 + lane * E; b < v1; b += U * S) {
+    uint4 r[U];
+    load(b, r);
+    batch(r);
   }
 #pragma unroll
   {  // warp combine: the warp's max first, then one fp64 rescale per lane and plain sums
