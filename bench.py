@@ -442,9 +442,10 @@ def run_e2e(args, c, obj, rlo, torch, cfg, logits, side, dev, stream, dist, key_
 
 
 def kernel_sass_hash(lib=None):
-    """sha256 of the SASS of every kernel in the library this run loaded
-    (cuobjdump -sass, addresses stripped): identifies the kernels a stored ncu
-    capture was taken from, independent of host-code or comment changes."""
+    """sha256 of the SASS of the vocab-pass kernels (vocab_ldg_kernel, every
+    instantiation) in the library this run loaded (cuobjdump -sass, addresses
+    stripped): identifies the kernels a stored ncu capture was taken from,
+    independent of host code, comments or changes to other kernels."""
     import hashlib
     import re
     import subprocess
@@ -454,8 +455,13 @@ def kernel_sass_hash(lib=None):
         out = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True, timeout=120).stdout
     except Exception:
         return None
-    body = "\n".join(re.sub(r"/\*[0-9a-f]{4,}\*/|/\* 0x[0-9a-f]+ \*/", "", ln).strip()
-                     for ln in out.splitlines() if "Function :" in ln or re.match(r"\s+/\*[0-9a-f]{4,}\*/", ln))
+    keep, lines = False, []
+    for ln in out.splitlines():
+        if "Function :" in ln:
+            keep = "vocab_ldg_kernel" in ln
+        if keep and ("Function :" in ln or re.match(r"\s+/\*[0-9a-f]{4,}\*/", ln)):
+            lines.append(re.sub(r"/\*[0-9a-f]{4,}\*/|/\* 0x[0-9a-f]+ \*/", "", ln).strip())
+    body = "\n".join(lines)
     return hashlib.sha256(body.encode()).hexdigest()[:16]
 
 
