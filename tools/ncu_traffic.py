@@ -1,6 +1,6 @@
 """Record the vocab kernel's DRAM traffic per launch from an `ncu --set full`
 capture into profiles/ncu_traffic.json, keyed by bench config and stamped with
-the SASS hash of the library the capture was taken from (bench.py uses the
+the SASS hash of the vocab-pass kernels the capture was taken from (bench.py uses the
 number as roofline.traffic only while the kernels are unchanged).
 
     python tools/ncu_traffic.py CFG REPORT.ncu-rep [LIB.so]
