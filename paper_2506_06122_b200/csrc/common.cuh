@@ -58,6 +58,14 @@ __device__ __forceinline__ void ld_stream256(const float4* p, float4& a, float4&
       : "l"(p));
 }
 
+// sm_100 256-bit streaming store (STG.E.256, evict-first): two 16-byte vectors
+// to 32 contiguous bytes; p must be 32-byte aligned.
+__device__ __forceinline__ void st_stream256(uint4* p, const uint4& a, const uint4& b) {
+  asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+               "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
+
 // ---- packed fp32x2 (sm_100 FFMA2 / FADD2: two fp32 lanes per instruction) ----
 using f2 = unsigned long long;
 __device__ __forceinline__ f2 pk2(float lo, float hi) {
