@@ -182,3 +182,62 @@ def test_random_update_pass_vs_oracle(env, case):
             continue
         want = O.logits_backward_row(rows[r], int(tokens.ravel()[r]), scale)
         assert np.abs(G[j] - want).max() <= 1e-5 * abs(scale) + 1e-12, (case, j)
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_random_long_rows_loss_pass_vs_oracle(env, case):
+    """Long bf16 rows (the lockstep kernels on a deferred offset for P = 2 / 3,
+    the lazy-max kernel for P = 1): random vocabularies >= 64 Ki (odd ones,
+    padded and unaligned strides), old / ref rows shifted against the actor
+    by up to +-90 nats, -inf masked entries, late spikes far above a thread's
+    first batch, whole rows shifted by hundreds of nats -- per-token log-probs
+    of every tensor and the entropy against the fp64 oracle."""
+    torch, rlo, obj = env
+    rng = np.random.default_rng(12000 + case)
+    V = int(rng.choice([65536, 65537, 100003, 131072, 152064]))
+    pad = int(rng.choice([0, 8, 1]))
+    stride = V + pad
+    P = [1, 2, 3][case % 3]
+    B, T = int(rng.integers(1, 4)), int(rng.integers(1, 5))
+    lengths = rng.integers(1, T + 1, B).astype(np.int32)
+    n = B * T
+    base = (rng.standard_normal((n, stride)) * float(rng.choice([1.0, 2.5, 4.0]))).astype(np.float32)
+    if rng.random() < 0.3:
+        base += float(rng.choice([-300.0, 150.0, 400.0]))
+    if rng.random() < 0.4:  # late spikes, far above the thread's first batch
+        for r in range(n):
+            base[r, int(rng.integers(V // 2, V))] += float(rng.choice([20.0, 45.0, 90.0]))
+    masked = rng.random() < 0.3
+    if masked:  # masked vocabulary entries, the same in every tensor
+        idx = rng.choice(V, V // 5, replace=False)
+        base[:, idx] = -np.inf
+    rows = [base]
+    for _ in range(P - 1):
+        off = float(rng.choice([0.0, 5.0, -5.0, 30.0, -30.0, 90.0, -90.0]))
+        rows.append((base + off + rng.standard_normal((n, stride)).astype(np.float32) * 0.3).astype(np.float32))
+    dev_rows = [dev(torch, r).to(torch.bfloat16)[:, :V] for r in rows]
+    host_rows = [np.ascontiguousarray(t.float().cpu().numpy()) for t in dev_rows]
+    tokens = np.zeros((B, T), np.int32)
+    for r in range(n):  # a finite logit (masked entries hold -inf)
+        fin = np.flatnonzero(np.isfinite(host_rows[0][r]))
+        tokens.ravel()[r] = int(rng.choice(fin))
+    cfg = rlo.TrainConfig(kl_coef=0.001, kl_estimator="k3")
+    kw = {}
+    kw.update(old_logits=dev_rows[1]) if P >= 2 else kw.update(
+        old_logprobs=dev(torch, rng.uniform(-9, -1, (B, T)).astype(np.float32)))
+    kw.update(ref_logits=dev_rows[2]) if P >= 3 else kw.update(
+        ref_logprobs=dev(torch, rng.uniform(-9, -1, (B, T)).astype(np.float32)))
+    adv = dev(torch, rng.uniform(-1, 1, (B, T)).astype(np.float32))
+    names = ("logp", "old_logp", "ref_logp")[:P]
+    outs = obj.ppo_gradient(cfg, dev(torch, tokens), dev(torch, lengths), dev_rows[0], adv,
+                            outputs=names + ("entropy",), **kw)
+    try:
+        obj.merge_gradients(cfg)
+    except rlo.TrainingError:  # ratios of rows shifted far apart can overflow, as in the reference
+        pass
+    m = (np.arange(T)[None, :] < lengths[:, None]).ravel()
+    for k, name in enumerate(names):
+        lp, ent, _ = O.forward_logprobs(host_rows[k], O.F32, V, V, B, T, lengths, tokens)
+        close_arr(outs[name].cpu().numpy().ravel()[m], lp[m], TOL, f"{name} case {case} V {V} pad {pad} P {P}")
+        if k == 0:
+            close_arr(outs["entropy"].cpu().numpy().ravel()[m], ent[m], 2e-5, f"entropy case {case}")
