@@ -22,7 +22,10 @@ namespace vocab {
 
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef RLO_VOCAB_THREADS  // CTA size (A/B; RLO_LDG_MIN_BLOCKS scales the other way)
+#define RLO_VOCAB_THREADS 256
+#endif
+constexpr int kThreads = RLO_VOCAB_THREADS;
 constexpr int kWarps = kThreads / 32;
 
 // Build-time knob for A/B library builds (make EXTRA="-D..."):
