@@ -22,16 +22,21 @@ namespace vocab {
 
 namespace {
 
-#ifndef RLO_VOCAB_THREADS  // CTA size (A/B; RLO_LDG_MIN_BLOCKS scales the other way)
-#define RLO_VOCAB_THREADS 256
+// CTA size per dtype (compile-time): bf16 rows are streamed by
+// ONE warp per row (CTAs of 32 threads, 32 per SM: no cross-warp reduction,
+// no barrier, 4736 rows in flight), fp32 rows by 256-thread CTAs (the fp32
+// pass reads 5% less with 32- or 64-thread CTAs, profiles/r2_vocab_ab.txt).
+#ifndef RLO_F32_THREADS
+#define RLO_F32_THREADS 256
 #endif
-constexpr int kThreads = RLO_VOCAB_THREADS;
-constexpr int kWarps = kThreads / 32;
-
+#ifndef RLO_BF16_THREADS
+#define RLO_BF16_THREADS 32
+#endif
 // Build-time knob for A/B library builds (make EXTRA="-D..."):
-// RLO_LDG_MIN_BLOCKS = __launch_bounds__ minimum CTAs per SM (register cap).
-#ifndef RLO_LDG_MIN_BLOCKS
-#define RLO_LDG_MIN_BLOCKS 4
+// RLO_LDG_THREADS_PER_SM = resident threads per SM the register cap of
+// __launch_bounds__ is sized for (1024: 64 registers).
+#ifndef RLO_LDG_THREADS_PER_SM
+#define RLO_LDG_THREADS_PER_SM 1024
 #endif
 // RLO_ENT_GUARD_ALWAYS = 1: the entropy row always runs the guarded math
 // (no redo path).
@@ -52,15 +57,15 @@ constexpr int kWarps = kThreads / 32;
 // actor max of the thread's first batch only; later batches take no max, test
 // or rescale at all -- the kernel's range checks on the finished shares redo
 // any share that left the safe range.
-// Thread tid's share is the vectors base + u * kThreads + tid -- the layout of
+// Thread tid's share is the vectors base + u * NTH + tid -- the layout of
 // stream_accumulate with the same U, so a redo covers exactly the share it
 // replaces (a 256-bit pair layout here would break that; it also read 0.6%
 // fewer bytes, profiles/r2_vocab_ab.txt call t).
-template <typename ET, int NT, int U, int MATH, bool DEF = false>
+template <int NTH, typename ET, int NT, int U, int MATH, bool DEF = false>
 __device__ __forceinline__ void lockstep_accumulate(const ET* const (&rows)[NT], int V, Acc (&acc)[NT]) {
   using VT = Vec<ET>;
   using VV = typename VT::V;
-  constexpr int kStep = kThreads * U;
+  constexpr int kStep = NTH * U;
   const int tid = threadIdx.x;
   const int nvec = V / VT::kElems;
   const int nfull = nvec / kStep * kStep;
@@ -90,7 +95,7 @@ __device__ __forceinline__ void lockstep_accumulate(const ET* const (&rows)[NT],
 #pragma unroll
     for (int k = 0; k < NT; ++k)
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[k][u] = ld_stream(reinterpret_cast<const VV*>(rows[k]) + base + u * kThreads + tid);
+      for (int u = 0; u < U; ++u) v[k][u] = ld_stream(reinterpret_cast<const VV*>(rows[k]) + base + u * NTH + tid);
     step(v);
   }
   if (nfull < nvec) {
@@ -99,14 +104,14 @@ __device__ __forceinline__ void lockstep_accumulate(const ET* const (&rows)[NT],
     for (int k = 0; k < NT; ++k)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int idx = nfull + u * kThreads + tid;
+        const int idx = nfull + u * NTH + tid;
         v[k][u] = idx < nvec ? ld_stream(reinterpret_cast<const VV*>(rows[k]) + idx) : VT::fill();
       }
     step(v);
   }
 #pragma unroll
   for (int k = 0; k < NT; ++k)
-    for (int i = nvec * VT::kElems + tid; i < V; i += kThreads) {
+    for (int i = nvec * VT::kElems + tid; i < V; i += NTH) {
       if (k == 0)
         acc_scalar<ET, true>(rows[k] + i, acc[k]);
       else
@@ -116,9 +121,12 @@ __device__ __forceinline__ void lockstep_accumulate(const ET* const (&rows)[NT],
 
 // U / PF: the layout of the entropy (actor) row; UN / PFN: the layout of the
 // other rows (old / ref, or the rows of a pass without entropy).
-template <typename ET, int NT, int U, bool PF, bool LOSS, bool ENT0, int MATH, bool LS = false, int UN = U,
+// NTH: threads per CTA (one row per CTA at a time); NTH = 32 finishes each
+// row inside the warp (no shared-memory reduction, no barrier).
+template <int NTH, typename ET, int NT, int U, bool PF, bool LOSS, bool ENT0, int MATH, bool LS = false, int UN = U,
           bool PFN = PF>
-__global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel(const VocabArgs a) {
+__global__ void __launch_bounds__(NTH, RLO_LDG_THREADS_PER_SM / NTH) vocab_ldg_kernel(const VocabArgs a) {
+  constexpr int kWarps = NTH / 32;
   __shared__ float red[2][kWarps][NT][3];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t nrows = (int64_t)a.B * a.T;
@@ -143,14 +151,14 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
         acc_init(acc[k]);
       }
       if (__all_sync(0xffffffffu, aligned)) {  // aligned is uniform per row anyway
-        lockstep_accumulate<ET, NT, U, MATH & kMathMask, (MATH & kMathDeferred) != 0>(rows, a.V, acc);
+        lockstep_accumulate<NTH, ET, NT, U, MATH & kMathMask, (MATH & kMathDeferred) != 0>(rows, a.V, acc);
         // Redo the actor share exactly (and guarded) on -inf logits (w = 0 * -inf)
         // or, under the deferred offset, when the share's max sat so far above
         // the offset (s >= 2^32, as the lazy max's cap) that the entropy's
         // log2 s - w/s would cancel too many bits.
         if (!(isfinite(acc[0].s) && isfinite(acc[0].w)) || ((MATH & kMathDeferred) && !(acc[0].s < kLazyCap))) {
           acc_init(acc[0]);
-          stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rows[0], a.V, acc[0]);
+          stream_accumulate<NTH, ET, U, PF, true, MATH | kMathGuard>(rows[0], a.V, acc[0]);
         }
 #pragma unroll
         for (int k = 1; k < NT; ++k)
@@ -161,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
           // ex2.approx.ftz flushed part of its mass to zero; NaN fails both.
           if (!(acc[k].s >= 0x1p-80f && acc[k].s < 0x1p100f)) {
             acc_init(acc[k]);
-            stream_accumulate<kThreads, ET, UN, PFN, false, MATH>(rows[k], a.V, acc[k]);
+            stream_accumulate<NTH, ET, UN, PFN, false, MATH>(rows[k], a.V, acc[k]);
           }
         goto reduce;
       }
@@ -172,25 +180,29 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
       const ET* rp = reinterpret_cast<const ET*>(a.logits[k]) + logits_off(a, k, row);
       if (k == 0 && ENT0) {
         if (RLO_ENT_GUARD_ALWAYS || sizeof(ET) == 4) {  // fp32 rows are memory-bound: one guarded body
-          stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, acc[k]);
+          stream_accumulate<NTH, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, acc[k]);
         } else if constexpr ((MATH & kMathDeferred) != 0) {
-          stream_checked<kThreads, ET, U, PF, true, MATH>(rp, a.V, acc[k]);
+          stream_checked<NTH, ET, U, PF, true, MATH>(rp, a.V, acc[k]);
         } else {
-          stream_accumulate<kThreads, ET, U, PF, true, MATH>(rp, a.V, acc[k]);
+          stream_accumulate<NTH, ET, U, PF, true, MATH>(rp, a.V, acc[k]);
           if (!(isfinite(acc[k].s) && isfinite(acc[k].w))) {
             // -inf logits in this thread's share: redo it guarded (the share
             // was just streamed, so the re-read mostly hits L2)
             acc_init(acc[k]);
-            stream_accumulate<kThreads, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, acc[k]);
+            stream_accumulate<NTH, ET, U, PF, true, MATH | kMathGuard>(rp, a.V, acc[k]);
           }
         }
       } else if constexpr ((MATH & kMathDeferred) != 0) {
-        stream_checked<kThreads, ET, UN, PFN, false, MATH>(rp, a.V, acc[k]);
+        stream_checked<NTH, ET, UN, PFN, false, MATH>(rp, a.V, acc[k]);
       } else {
-        stream_accumulate<kThreads, ET, UN, PFN, false, MATH>(rp, a.V, acc[k]);
+        stream_accumulate<NTH, ET, UN, PFN, false, MATH>(rp, a.V, acc[k]);
       }
     }
   reduce:
+    if constexpr (kWarps == 1) {  // the row's warp combines its lanes and finishes
+      row_finish_acc<NT, LOSS, ENT0>(a, acc, row, tok, oov, ztok, lane);
+      continue;
+    }
 #pragma unroll
     for (int k = 0; k < NT; ++k) {
       if (k == 0 && ENT0)
@@ -212,13 +224,14 @@ __global__ void __launch_bounds__(kThreads, RLO_LDG_MIN_BLOCKS) vocab_ldg_kernel
 template <typename ET, int NT, bool LOSS, bool ENT0, int MATH, int U, bool PF, bool LS = false, int UN = U,
           bool PFN = PF>
 cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
-  auto kern = vocab_ldg_kernel<ET, NT, U, PF, LOSS, ENT0, MATH, LS, UN, PFN>;
+  constexpr int NTH = sizeof(ET) == 4 ? RLO_F32_THREADS : RLO_BF16_THREADS;
+  auto kern = vocab_ldg_kernel<NTH, ET, NT, U, PF, LOSS, ENT0, MATH, LS, UN, PFN>;
   const int64_t nrows = (int64_t)a.B * a.T;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTH, 0);
   int64_t grid = (int64_t)num_sms * (per_sm < 1 ? 1 : per_sm);
   if (grid > nrows) grid = nrows;
-  kern<<<(int)grid, kThreads, 0, s>>>(a);
+  kern<<<(int)grid, NTH, 0, s>>>(a);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
