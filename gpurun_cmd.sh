@@ -1,10 +1,1 @@
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -rf 2>&1 | tail -4
-AB_P1=1 bash tools/ab_bench.sh ah 2 cur w1 | tee gpurun_out/r2ah_ab.txt
-for r in 1 2; do for L in cur w1; do
-RLO_LIB=$PWD/paper_2506_06122_b200/lib/variants/librlo_$L.so timeout 300 python tools/bench_update.py --cases bf16_32k --forms two_pass --iters 200 2>&1 | python3 -c "
-import json,sys
-for l in sys.stdin:
-    try: d=json.loads(l)
-    except Exception: continue
-    print('$L r$r', d['case'], 'loss_ms', round(d['loss_ms'],3), 'loss_gbs', round(d['loss_gbs']))"
-done; done | tee -a gpurun_out/r2ah_ab.txt
+AB_P1=1 bash tools/ab_bench.sh ai 2 cur u2 u4 p1u8 | tee gpurun_out/r2ai_ab.txt
