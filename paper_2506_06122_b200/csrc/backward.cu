@@ -16,7 +16,10 @@
 namespace rlo {
 namespace {
 
-constexpr int kBwThreads = 256;
+#ifndef RLO_BW_THREADS
+#define RLO_BW_THREADS 256
+#endif
+constexpr int kBwThreads = RLO_BW_THREADS;
 // RLO_BW256 = 1 (default): bf16 -> bf16 rows as 32-byte vector pairs (LDG.256 +
 // STG.256): +3.4% on the Qwen-vocabulary backward (profiles/r2_update_step.txt).
 #ifndef RLO_BW256

@@ -49,7 +49,10 @@
 namespace rlo {
 namespace {
 
-constexpr int kDecWarps = 8;
+#ifndef RLO_DEC_WARPS  // warps per row (one CTA per row)
+#define RLO_DEC_WARPS 8
+#endif
+constexpr int kDecWarps = RLO_DEC_WARPS;
 
 // rng::mix / keyed_double (rng.hpp:15-31, 82-85), restated bit-for-bit.
 __device__ __forceinline__ uint64_t splitmix(uint64_t& state) {
