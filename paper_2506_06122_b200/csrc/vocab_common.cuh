@@ -513,7 +513,9 @@ __device__ __forceinline__ void stream_checked(const ET* __restrict__ row, int V
   if constexpr (kDeferred || ENT) {
     // deferred: overflowed or not finite; lazy / exact entropy rows: -inf
     // logits make the unguarded e * t = 0 * -inf NaN (w - w != 0 for inf / NaN)
-    const bool bad = kDeferred ? (!(a.s < kDeferCap) || (ENT && !(a.w - a.w == 0.f)))
+    // (entropy rows: s < 2^32 as the lazy cap -- a share max far above the
+    // offset would cancel the bits of log2 s - w/s)
+    const bool bad = kDeferred ? (!(a.s < (ENT ? kLazyCap : kDeferCap)) || (ENT && !(a.w - a.w == 0.f)))
                                : !(isfinite(a.s) && isfinite(a.w));
     if (bad) {
       acc_init(a);
