@@ -340,13 +340,15 @@ def test_bf16_lockstep_offsets(env, off_old, off_ref, V):
 LS_FIRST = 3 * 256 * 8  # elements in the long-row lockstep kernel's first batch (U = 3 vectors x 256 threads)
 
 
+@pytest.mark.parametrize("pad", [0, 1])
 @pytest.mark.parametrize("gap", [0.0, 5.0, 10.0, 14.0, 40.0, "spike", "masked", "shift250", "shift300", "shift-400"])
-def test_bf16_long_lockstep_deferred_offset(env, gap):
+def test_bf16_long_lockstep_deferred_offset(env, gap, pad):
     """The long-row lockstep kernel (bf16, V = 152064, P = 3) sums every batch
     after a thread's first against that first batch's actor max.  Rows whose
     later elements sit `gap` nats above the first batch: below the redo cap
     (s < 2^32) the entropy's log2 s - w/s cancels the gap's bits and must stay
     within 1e-5; above it (gap 40, one +60 spike) the share is redone exactly;
+    pad = 1: the same rows off 16-byte alignment (the per-tensor fallback);
     "masked": a third of the actor row is -inf (masked vocabulary: guarded
     redo); "shiftX": whole rows X nats off zero (the packed-bf16 clamp of the
     polynomial lanes holds for offsets below 256 nats, larger ones keep the
@@ -368,6 +370,11 @@ def test_bf16_long_lockstep_deferred_offset(env, gap):
     if gap == "masked":
         tensors[1] = np.where(np.isinf(rows), rows, tensors[1])
     pairs = [bf16_bits(torch, r) for r in tensors]
+    if pad:  # a row stride of V + 1: rows off 16-byte alignment take the kernel's per-tensor deferred fallback
+        for i, (d, h) in enumerate(pairs):
+            full = torch.zeros(B * T, V + pad, dtype=torch.bfloat16, device="cuda")
+            full[:, :V] = d
+            pairs[i] = (full[:, :V], h)
     tokens = rng.integers(LS_FIRST, V, (B, T)).astype(np.int32)
     if gap == "masked":
         tokens = np.array([[int(np.argmax(r)) for r in rows]], np.int32).reshape(B, T)
