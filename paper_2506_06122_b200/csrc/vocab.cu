@@ -3,10 +3,11 @@
 //
 // Replaces the reference's per-position log-softmax + gather
 // (policy.cpp:116-122, :227; forward_logprobs :210-233) and the loss part of
-// ppo_gradient (:355-374).  One sm_100a kernel template: persistent CTAs of
-// 256 threads streaming rows with U 128-bit ld.global.nc.L1::no_allocate
-// loads in flight per thread; the math and the epilogue live in
-// vocab_common.cuh; the softmax is never written.
+// ppo_gradient (:355-374).  One sm_100a kernel template: persistent CTAs
+// streaming rows with U 128-bit ld.global.nc.L1::no_allocate loads in flight
+// per thread -- one warp per row for bf16 (32-thread CTAs, the row finished
+// inside the warp), 256 threads per row for fp32; the math and the epilogue
+// live in vocab_common.cuh; the softmax is never written.
 //
 // The library ships exactly one instantiation per (dtype, tensors, mode,
 // entropy) — the measured defaults (profiles/r1_vocab_sweep.txt);
@@ -250,7 +251,9 @@ cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
 //        the thread's first batch; no per-batch max, test or rescale):
 //        +3-4% over the per-tensor lazy-max streams at the power cap
 //        (profiles/r2_vocab_ab.txt); the 2-tensor loss pass (actor + old or
-//        ref) over long rows the same way (+3%).
+//        ref) over long rows the same way (+3%);
+//  bf16 rows one warp per row (RLO_BF16_THREADS = 32): +2.9% on cfg3, +4.5%
+//        on the 1-tensor pass, +19% on short 3-tensor rows (calls ae-ah).
 #ifndef RLO_F32_MATH
 #define RLO_F32_MATH 1
 #endif
