@@ -1,1 +1,1 @@
-AB_P1=1 bash tools/ab_bench.sh al 2 cur p1m4 m5 m9 | tee gpurun_out/r2al_ab.txt
+AB_P1=1 AB_ARGS="--config 2" bash tools/ab_bench.sh am 3 cur f128 f512 | tee gpurun_out/r2am_ab.txt
