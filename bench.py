@@ -441,11 +441,24 @@ def run_e2e(args, c, obj, rlo, torch, cfg, logits, side, dev, stream, dist, key_
             "d2h_bytes_per_step": hb_out + 64, "api": api, "ms_per_step": 1e3 * el / args.steps}
 
 
-def kernel_sass_hash(lib=None):
-    """sha256 of the SASS of the vocab-pass kernels (vocab_ldg_kernel, every
-    instantiation) in the library this run loaded (cuobjdump -sass, addresses
-    stripped): identifies the kernels a stored ncu capture was taken from,
-    independent of host code, comments or changes to other kernels."""
+def kernel_sig(name):
+    """Normalised template signature of a vocab_ldg_kernel instantiation from
+    an ncu or c++filt kernel name: 'vocab_ldg_kernel<32,__nv_bfloat16,3,...>'
+    (bools as 0 / 1, no spaces)."""
+    import re
+    m = re.search(r"vocab_ldg_kernel<[^()]*>", name)
+    if not m:
+        return None
+    sig = m.group(0).replace(" ", "").replace("true", "1").replace("false", "0")
+    return sig.replace("(anonymousnamespace)::", "")
+
+
+def kernel_sass_hash(lib=None, sig=None):
+    """sha256 of the SASS of one vocab-pass kernel instantiation (`sig`, see
+    kernel_sig; every vocab_ldg_kernel instantiation when None) in the
+    library this run loaded (cuobjdump -sass, addresses stripped): identifies
+    the kernel a stored ncu capture was taken from, independent of host code,
+    comments or changes to other kernels."""
     import hashlib
     import re
     import subprocess
@@ -453,16 +466,21 @@ def kernel_sass_hash(lib=None):
     lib = lib or _abi.LIB_PATH
     try:
         out = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True, timeout=120).stdout
+        names = subprocess.run(["c++filt"], input="\n".join(re.findall(r"Function : (\S+)", out)),
+                               capture_output=True, text=True, timeout=60).stdout.splitlines()
     except Exception:
         return None
+    demangled = dict(zip(re.findall(r"Function : (\S+)", out), names))
     keep, lines = False, []
     for ln in out.splitlines():
         if "Function :" in ln:
-            keep = "vocab_ldg_kernel" in ln
+            fn = demangled.get(ln.split("Function :")[1].strip(), "")
+            keep = "vocab_ldg_kernel" in fn and (sig is None or kernel_sig(fn) == sig)
         if keep and ("Function :" in ln or re.match(r"\s+/\*[0-9a-f]{4,}\*/", ln)):
             lines.append(re.sub(r"/\*[0-9a-f]{4,}\*/|/\* 0x[0-9a-f]+ \*/", "", ln).strip())
-    body = "\n".join(lines)
-    return hashlib.sha256(body.encode()).hexdigest()[:16]
+    if not lines:
+        return None
+    return hashlib.sha256("\n".join(lines).encode()).hexdigest()[:16]
 
 
 def traffic_from_profile(cfg_id):
@@ -478,8 +496,8 @@ def traffic_from_profile(cfg_id):
     v = d.get(f"cfg{cfg_id}")
     if v is None:
         return None, "no capture for this config"
-    if v.get("sass_hash") != kernel_sass_hash():
-        return None, "capture is from other kernels (SASS hash differs: stale): not used"
+    if v.get("sass_hash") is None or v.get("sass_hash") != kernel_sass_hash(sig=v.get("kernel_sig")):
+        return None, "capture is from another build of this kernel (SASS hash differs: stale): not used"
     return v.get("bytes_per_launch"), f"ncu capture {v.get('capture', '')} (kernel SASS {v.get('sass_hash')})"
 
 

@@ -1,6 +1,6 @@
 """Record the vocab kernel's DRAM traffic per launch from an `ncu --set full`
 capture into profiles/ncu_traffic.json, keyed by bench config and stamped with
-the SASS hash of the vocab-pass kernels the capture was taken from (bench.py uses the
+the SASS hash of the vocab-pass kernel instantiation the capture was taken from (bench.py uses the
 number as roofline.traffic only while the kernels are unchanged).
 
     python tools/ncu_traffic.py CFG REPORT.ncu-rep [LIB.so]
@@ -44,7 +44,8 @@ def main():
     d[f"cfg{cfg}"] = {"bytes_per_launch": val["dram__bytes_read.sum"] + val["dram__bytes_write.sum"],
                       "dram_read": val["dram__bytes_read.sum"], "dram_write": val["dram__bytes_write.sum"],
                       "launch_s_under_ncu": val["gpu__time_duration.sum"], "kernel": name,
-                      "capture": os.path.basename(rep), "sass_hash": bench.kernel_sass_hash(lib)}
+                      "capture": os.path.basename(rep), "kernel_sig": bench.kernel_sig(name),
+                      "sass_hash": bench.kernel_sass_hash(lib, bench.kernel_sig(name))}
     json.dump(d, open(p, "w"), indent=1)
     print(json.dumps(d[f"cfg{cfg}"]))
 
