@@ -243,20 +243,17 @@ cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
 // Compile-time defaults per dtype (A/B builds override them):
 //  fp32: mix 1 (packed FFMA2/FADD2, MUFU.EX2), U = 8 (128 B in flight per
 //        thread), entropy row always guarded (memory-bound: one body);
-//  bf16: mix 7 = mix 6 (degree-4 FMA-pipe exp2 on 1 of 4 old/ref element
-//        pairs, entropy row all MUFU) + the lazy running max, U = 4 with the
-//        next batch in flight (software prefetch);
-//  bf16 3-tensor loss pass over short rows (< 128 KB): mix 6 with the three
-//        tensors streamed in lockstep on the actor's running max, U = 2 per
-//        tensor (one cold start per row instead of three);
-//  bf16 3-tensor loss pass over long rows (cfg 3-5, V = 152064): mix 6 in
-//        lockstep, U = 3 per tensor, on a deferred offset (the actor max of
-//        the thread's first batch; no per-batch max, test or rescale):
-//        +3-4% over the per-tensor lazy-max streams at the power cap
-//        (profiles/r2_vocab_ab.txt); the 2-tensor loss pass (actor + old or
-//        ref) over long rows the same way (+3%);
-//  bf16 rows one warp per row (RLO_BF16_THREADS = 32): +2.9% on cfg3, +4.5%
-//        on the 1-tensor pass, +19% on short 3-tensor rows (calls ae-ah).
+//  bf16 loss pass with 2 or 3 logits tensors (cfg 3-5 and every bf16
+//        P >= 2 row): the tensors of a token streamed in lockstep, U = 3
+//        vectors of each per batch, one warp per row, on a deferred offset
+//        (the actor max of the lane's first batch; no per-batch max, test or
+//        rescale), mix 6 (degree-4 FMA-pipe exp2 on 1 of 4 old/ref element
+//        pairs, the entropy row all MUFU): +3-4% over per-tensor lazy-max
+//        streams on Qwen rows, +7% over the round-2 short-row lockstep
+//        (shared running max, U = 2) on V = 32000 rows (profiles/r2_vocab_ab.txt);
+//  bf16 1-tensor passes (P = 1 loss, forward_logprobs): mix 7 = mix 6 + the
+//        lazy running max, U = 4 with the next batch in flight (software
+//        prefetch), one warp per row.
 #ifndef RLO_F32_MATH
 #define RLO_F32_MATH 1
 #endif
@@ -278,44 +275,25 @@ cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
 #ifndef RLO_BF16_MATH_P1
 #define RLO_BF16_MATH_P1 RLO_BF16_MATH
 #endif
-#ifndef RLO_BF16_LONG_LS
-#define RLO_BF16_LONG_LS 3
+#ifndef RLO_BF16_LS_U  // lockstep vectors per tensor per batch (0: per-tensor lazy streams, A/B)
+#define RLO_BF16_LS_U 3
 #endif
-#ifndef RLO_BF16_LS_P2
-#define RLO_BF16_LS_P2 1
+#ifndef RLO_BF16_LS_MATH
+#define RLO_BF16_LS_MATH 6
 #endif
-#ifndef RLO_BF16_LONG_LS_MATH
-#define RLO_BF16_LONG_LS_MATH RLO_BF16_SHORT_MATH
-#endif
-#ifndef RLO_BF16_SHORT_MATH
-#define RLO_BF16_SHORT_MATH 6
-#endif
-constexpr int kLongRowV = 65536;  // bf16 rows of >= 128 KB count as long
 
 template <typename ET, int NT, bool LOSS, bool ENT0>
 cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
   if ((int64_t)a.B * a.T == 0) return cudaSuccess;
   if constexpr (sizeof(ET) == 4) {
     return launch_ldg<ET, NT, LOSS, ENT0, RLO_F32_MATH, 8, false>(a, num_sms, s);
+  } else if constexpr (NT >= 2 && LOSS && RLO_BF16_LS_U != 0) {  // lockstep on a deferred offset
+    return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_LS_MATH | kMathDeferred, RLO_BF16_LS_U, false, true>(a, num_sms, s);
   } else {
-    if constexpr (NT == 3 && LOSS && RLO_BF16_LONG_LS != 0) {  // lockstep: short rows / long rows
-      if (a.V < kLongRowV) return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_SHORT_MATH, 2, false, true>(a, num_sms, s);
-      return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_LONG_LS_MATH | kMathDeferred, RLO_BF16_LONG_LS, false, true>(
-          a, num_sms, s);
-    } else if constexpr (NT == 2 && LOSS && RLO_BF16_LONG_LS != 0 && RLO_BF16_LS_P2) {  // P = 2: long rows lockstep
-      if (a.V >= kLongRowV)
-        return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_LONG_LS_MATH | kMathDeferred, RLO_BF16_LONG_LS, false, true>(
-            a, num_sms, s);
-      return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, false, RLO_BF16_UN, RLO_BF16_PFN>(
-          a, num_sms, s);
-    } else {
-      if constexpr (NT == 3 && LOSS)
-        if (a.V < kLongRowV) return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_SHORT_MATH, 2, false, true>(a, num_sms, s);
-      if constexpr (NT == 1 && LOSS && ENT0 && RLO_BF16_MATH_P1 != RLO_BF16_MATH)  // A/B: actor-only loss pass
-        return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH_P1, RLO_BF16_U, RLO_BF16_PF>(a, num_sms, s);
-      return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, false, RLO_BF16_UN, RLO_BF16_PFN>(
-          a, num_sms, s);
-    }
+    if constexpr (NT == 1 && LOSS && ENT0 && RLO_BF16_MATH_P1 != RLO_BF16_MATH)  // A/B: actor-only loss pass
+      return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH_P1, RLO_BF16_U, RLO_BF16_PF>(a, num_sms, s);
+    return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, false, RLO_BF16_UN, RLO_BF16_PFN>(
+        a, num_sms, s);
   }
 }
 

@@ -9,7 +9,7 @@ row-strided outputs (gradients) also keep their padding columns.  Each launch
 runs twice and must give bitwise-identical outputs (a shared-memory or DSMEM
 race, or a missing barrier, shows up as run-to-run differences).  Small
 shapes, every shipped kernel: the vocab pass (fp32 / bf16, long rows with the
-lazy max, short rows in lockstep, unaligned rows), the fused update pass
+lazy max, lockstep on a deferred offset, unaligned rows), the fused update pass
 (cluster + DSMEM), the backward epilogue, the advantage scans, decode."""
 import numpy as np
 import pytest

@@ -14,11 +14,10 @@ rlo_objective_step_host_mb):
   rows that defeat a lazy max / deferred offset: every element far below one
   spike that sits in a polynomial lane (the .y word of a uint4), actor rows
   whose later batches sit 5-40 nats above the first, -inf masked entries;
-* bf16 P = 2 over long rows: the same lockstep kernel with two tensors;
-* bf16 P = 1, and P = 2 over short rows: the lazy-running-max kernel (mix 7);
-* bf16 V < 65536, P = 3: the short-row lockstep kernel (old/ref sums on the
-  actor's running max); both lockstep kernels with old/ref rows far above and
-  far below the actor's;
+* bf16 P = 2: the same lockstep kernel with two tensors; both lockstep
+  kernels at V = 32000 too, with old/ref rows far above and far below the
+  actor's;
+* bf16 P = 1: the lazy-running-max kernel (mix 7);
 * the fp32 and bf16 forward_logprobs instantiations with and without entropy.
 
 Tolerance (north_star): |gpu - oracle| <= 1e-5 * max(1, |oracle|) for
@@ -309,9 +308,8 @@ def test_bf16_spike_above_running_max_forward_logprobs(env, entropy):
 @pytest.mark.parametrize("V", [32000, QWEN_V])
 @pytest.mark.parametrize("off_old,off_ref", [(200.0, -80.0), (30.0, -40.0), (-300.0, 120.0)])
 def test_bf16_lockstep_offsets(env, off_old, off_ref, V):
-    """bf16 P = 3 rows take the lockstep kernels (short rows: on the actor's
-    running max; long rows: on the deferred offset), whose old/ref sums ride
-    on the actor's offset: old/ref rows far above it (overflow side) or far
+    """bf16 P = 3 rows take the lockstep kernel on a deferred offset (any V),
+    whose old/ref sums ride on the actor's offset: old/ref rows far above it (overflow side) or far
     below it (ex2.approx.ftz flushes the bulk of the row) must be redone with
     their own max."""
     torch, rlo, obj = env
@@ -396,9 +394,8 @@ def test_bf16_long_lockstep_deferred_offset(env, gap, pad):
 @pytest.mark.parametrize("P", [1, 2])
 def test_bf16_p1_p2_kernels(env, P, V):
     """bf16 loss pass with one or two logits tensors (old / ref log-probs
-    precomputed) against the oracle: P = 1 (any V) and P = 2 short rows take
-    the lazy-running-max kernel (mix 7), P = 2 long rows the lockstep kernel
-    on a deferred offset; at V = 152064 the old rows of the first tokens are
+    precomputed) against the oracle: P = 1 takes the lazy-running-max kernel
+    (mix 7), P = 2 the lockstep kernel on a deferred offset; at V = 152064 the old rows of the first tokens are
     the spike rows that defeat a lazy max."""
     torch, rlo, obj = env
     rng = np.random.default_rng(90 + P)
@@ -477,12 +474,11 @@ def test_bf16_row_alignments(env, pad):
 
 @pytest.mark.parametrize("V,stride", [(100003, 100008), (70001, 70001), (65536, 65536), (65535, 65544)])
 def test_bf16_long_rows_odd_vocab(env, V, stride):
-    """Long bf16 rows (>= 64 Ki elements take the long-row lockstep kernel)
-    with a vocabulary that is not a multiple of the 16-byte vector: aligned
-    rows (stride a multiple of 8) run the lockstep batches, the partial batch
-    and the scalar tail; a contiguous odd vocabulary misaligns every other row
-    (per-tensor fallback inside the same kernel); V = 65536 / 65535 sit at the
-    short/long boundary.  P = 3 loss pass against the oracle."""
+    """bf16 rows in the lockstep kernel with a vocabulary that is not a
+    multiple of the 16-byte vector: aligned rows (stride a multiple of 8) run
+    the lockstep batches, the partial batch and the scalar tail; a contiguous
+    odd vocabulary misaligns every other row (per-tensor fallback inside the
+    same kernel).  P = 3 loss pass against the oracle."""
     torch, rlo, obj = env
     rng = np.random.default_rng(V)
     B, T = 2, 3
