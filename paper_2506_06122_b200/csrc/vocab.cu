@@ -42,6 +42,12 @@ namespace {
 #ifndef RLO_LDG_THREADS_PER_SM
 #define RLO_LDG_THREADS_PER_SM 1024
 #endif
+// The bf16 lockstep kernel (P >= 2): 768 resident threads per SM (24 rows in
+// flight per SM, 80 registers): +1.5% on cfg3 against 1024 (the 1-tensor
+// pass loses 2.3% there and keeps 1024; profiles/r2_vocab_ab.txt calls ap-aq).
+#ifndef RLO_BF16_LS_THREADS_PER_SM
+#define RLO_BF16_LS_THREADS_PER_SM 768
+#endif
 // RLO_ENT_GUARD_ALWAYS = 1: the entropy row always runs the guarded math
 // (no redo path).
 #ifndef RLO_ENT_GUARD_ALWAYS
@@ -129,7 +135,8 @@ __device__ __forceinline__ void lockstep_accumulate(const ET* const (&rows)[NT],
 // row inside the warp (no shared-memory reduction, no barrier).
 template <int NTH, typename ET, int NT, int U, bool PF, bool LOSS, bool ENT0, int MATH, bool LS = false, int UN = U,
           bool PFN = PF>
-__global__ void __launch_bounds__(NTH, RLO_LDG_THREADS_PER_SM / NTH) vocab_ldg_kernel(const VocabArgs a) {
+__global__ void __launch_bounds__(NTH, (LS && sizeof(ET) == 2 ? RLO_BF16_LS_THREADS_PER_SM : RLO_LDG_THREADS_PER_SM) / NTH)
+    vocab_ldg_kernel(const VocabArgs a) {
   constexpr int kWarps = NTH / 32;
   __shared__ float red[2][kWarps][NT][3];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
