@@ -24,13 +24,13 @@ namespace vocab {
 namespace {
 
 // CTA size per dtype (compile-time): bf16 rows are streamed by
-// ONE warp per row (CTAs of 32 threads, 32 per SM: no cross-warp reduction,
-// no barrier, 4736 rows in flight), fp32 rows by 256-thread CTAs (the fp32
-// pass reads 5% less with 32- or 64-thread CTAs, profiles/r2_vocab_ab.txt).
+// ONE warp per row (CTAs of 32 threads: no cross-warp reduction, no barrier),
+// fp32 rows by 256-thread CTAs (the 2/3-tensor fp32 passes read 3-5% less
+// with 32-128-thread CTAs, profiles/r2_vocab_ab.txt calls ag, am).
 #ifndef RLO_F32_THREADS
 #define RLO_F32_THREADS 256
 #endif
-#ifndef RLO_F32_THREADS_1T  // fp32 1-tensor passes (P = 1 loss, forward_logprobs): +3.7% at 128 (call am)
+#ifndef RLO_F32_THREADS_1T  // fp32 1-tensor passes (P = 1 loss, forward_logprobs): +2.8% at 128 (call an)
 #define RLO_F32_THREADS_1T 128
 #endif
 #ifndef RLO_BF16_THREADS
@@ -43,8 +43,9 @@ namespace {
 #define RLO_LDG_THREADS_PER_SM 1024
 #endif
 // The bf16 lockstep kernel (P >= 2): 768 resident threads per SM (24 rows in
-// flight per SM, 80 registers): +1.5% on cfg3 against 1024 (the 1-tensor
-// pass loses 2.3% there and keeps 1024; profiles/r2_vocab_ab.txt calls ap-aq).
+// flight per SM, 80 registers, no spills): +2.1% on cfg3 against 1024 (the
+// 1-tensor pass and the fp32 passes lose at 768 and keep 1024;
+// profiles/r2_vocab_ab.txt calls ap-at).
 #ifndef RLO_BF16_LS_THREADS_PER_SM
 #define RLO_BF16_LS_THREADS_PER_SM 768
 #endif
@@ -57,13 +58,12 @@ namespace {
 // Lockstep streams (LS): the NT tensors of a row are streamed together, U
 // vectors of each per batch, and the old/ref states share the actor's running
 // max instead of taking their own chunk maxima (saves the per-chunk max and
-// rescale on NT-1 tensors — the bf16 pass is bound by SM power, so fewer
-// instructions per byte buy clock).  A thread's old/ref share whose sum on the
+// rescale on NT-1 tensors; one cold start per row).  A thread's old/ref share whose sum on the
 // shared max leaves [2^-80, 2^100) — an element far above the actor's max, or
 // a tensor so far below it that flushed terms matter — is redone with the
 // tensor's own max (the kernel below).  Rows must all be 16-byte aligned
 // (else the sequential streams).
-// DEF (deferred offset; the shipped long-row layout): the shared offset is the
+// DEF (deferred offset; the shipped layout): the shared offset is the
 // actor max of the thread's first batch only; later batches take no max, test
 // or rescale at all -- the kernel's range checks on the finished shares redo
 // any share that left the safe range.
