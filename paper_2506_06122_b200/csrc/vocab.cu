@@ -49,6 +49,9 @@ namespace {
 #ifndef RLO_BF16_LS_THREADS_PER_SM
 #define RLO_BF16_LS_THREADS_PER_SM 768
 #endif
+#ifndef RLO_BF16_PAIR_THREADS_PER_SM
+#define RLO_BF16_PAIR_THREADS_PER_SM 768
+#endif
 // RLO_ENT_GUARD_ALWAYS = 1: the entropy row always runs the guarded math
 // (no redo path).
 #ifndef RLO_ENT_GUARD_ALWAYS
@@ -232,6 +235,111 @@ __global__ void __launch_bounds__(NTH, (LS && sizeof(ET) == 2 ? RLO_BF16_LS_THRE
   }
 }
 
+// The bf16 1-tensor loss pass (P = 1: old / ref log-probs precomputed): TWO
+// rows per warp in lockstep (consecutive tokens), U = 5 vectors of each per
+// batch, each row on its own deferred offset (the max of its first batch),
+// 768 resident threads per SM: +2.9% over the lazy-max stream with prefetch
+// (profiles/r2_vocab_ab.txt calls ax-ay).  A row whose share leaves the safe
+// range (non-finite, or s >= 2^32: the entropy's cancellation) is redone
+// exactly and guarded; a pair with an inactive or misaligned row streams its
+// rows one by one (exact, guarded).
+template <typename ET, int U, int MATH>
+__device__ __forceinline__ void pair_accumulate(const ET* const (&rows)[2], int V, Acc (&acc)[2]) {
+  using VT = Vec<ET>;
+  using VV = typename VT::V;
+  constexpr int kStep = 32 * U;
+  const int lane = threadIdx.x & 31;
+  const int nvec = V / VT::kElems;
+  const int nfull = nvec / kStep * kStep;
+  auto step = [&](const VV (&v)[2][U]) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (acc[k].mL > kLazyMin)
+        VT::template accumulate<U, true, MATH | kMathNoMax>(v[k], acc[k]);
+      else
+        VT::template accumulate<U, true, MATH>(v[k], acc[k]);
+    }
+  };
+  for (int base = 0; base < nfull; base += kStep) {
+    VV v[2][U];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[k][u] = ld_stream(reinterpret_cast<const VV*>(rows[k]) + base + u * 32 + lane);
+    step(v);
+  }
+  if (nfull < nvec) {
+    VV v[2][U];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = nfull + u * 32 + lane;
+        v[k][u] = idx < nvec ? ld_stream(reinterpret_cast<const VV*>(rows[k]) + idx) : VT::fill();
+      }
+    step(v);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+    for (int i = nvec * VT::kElems + lane; i < V; i += 32) acc_scalar<ET, true>(rows[k] + i, acc[k]);
+}
+
+template <typename ET, int U, int MATH>
+__global__ void __launch_bounds__(32, RLO_BF16_PAIR_THREADS_PER_SM / 32) vocab_pair_kernel(const VocabArgs a) {
+  const int lane = threadIdx.x;
+  const int64_t nrows = (int64_t)a.B * a.T, npairs = (nrows + 1) / 2;
+  for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+    const int64_t r[2] = {2 * pr, 2 * pr + 1};
+    bool act[2];
+    int tok[2] = {0, 0};
+    bool oov[2] = {false, false};
+    float ztok[2][1];
+    const ET* rp[2];
+    Acc acc[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      act[k] = r[k] < nrows && row_active<true>(a, r[k], lane == 0);
+      if (r[k] < nrows && !act[k] && lane == 0) write_inactive<true>(a, r[k]);
+      if (act[k] && lane == 0) gather_token<ET, 1>(a, r[k], tok[k], oov[k], ztok[k]);
+      rp[k] = reinterpret_cast<const ET*>(a.logits[0]) + (r[k] < nrows ? logits_off(a, 0, r[k]) : 0);
+      acc_init(acc[k]);
+    }
+    const bool aligned = ((reinterpret_cast<uintptr_t>(rp[0]) | reinterpret_cast<uintptr_t>(rp[1])) & 15u) == 0;
+    if (act[0] && act[1] && aligned) {
+      pair_accumulate<ET, U, MATH>(rp, a.V, acc);
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if (!(isfinite(acc[k].s) && isfinite(acc[k].w)) || !(acc[k].s < kLazyCap)) {
+          acc_init(acc[k]);
+          stream_accumulate<32, ET, U, false, true, MATH | kMathGuard>(rp[k], a.V, acc[k]);
+        }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if (act[k]) stream_accumulate<32, ET, U, false, true, MATH | kMathGuard>(rp[k], a.V, acc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (act[k]) {
+        Acc c[1] = {acc[k]};
+        row_finish_acc<1, true, true>(a, c, r[k], tok[k], oov[k], ztok[k], lane);
+      }
+  }
+}
+
+template <typename ET, int U, int MATH>
+cudaError_t launch_pair(const VocabArgs& a, int num_sms, cudaStream_t s) {
+  auto kern = vocab_pair_kernel<ET, U, MATH>;
+  const int64_t npairs = ((int64_t)a.B * a.T + 1) / 2;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, 0);
+  int64_t grid = (int64_t)num_sms * (per_sm < 1 ? 1 : per_sm);
+  if (grid > npairs) grid = npairs;
+  kern<<<(int)grid, 32, 0, s>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
 template <typename ET, int NT, bool LOSS, bool ENT0, int MATH, int U, bool PF, bool LS = false, int UN = U,
           bool PFN = PF>
 cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
@@ -258,9 +366,9 @@ cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
 //        pairs, the entropy row all MUFU): +3-4% over per-tensor lazy-max
 //        streams on Qwen rows, +7% over the round-2 short-row lockstep
 //        (shared running max, U = 2) on V = 32000 rows (profiles/r2_vocab_ab.txt);
-//  bf16 1-tensor passes (P = 1 loss, forward_logprobs): mix 7 = mix 6 + the
-//        lazy running max, U = 4 with the next batch in flight (software
-//        prefetch), one warp per row.
+//  bf16 P = 1 loss pass: two rows per warp in lockstep (vocab_pair_kernel);
+//  bf16 forward_logprobs: mix 7 = mix 6 + the lazy running max, U = 4 with
+//        the next batch in flight (software prefetch), one warp per row.
 #ifndef RLO_F32_MATH
 #define RLO_F32_MATH 1
 #endif
@@ -285,6 +393,9 @@ cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
 #ifndef RLO_BF16_LS_U  // lockstep vectors per tensor per batch (0: per-tensor lazy streams, A/B)
 #define RLO_BF16_LS_U 3
 #endif
+#ifndef RLO_BF16_PAIR_U  // 0: the lazy-max stream (A/B)
+#define RLO_BF16_PAIR_U 5
+#endif
 #ifndef RLO_BF16_LS_MATH
 #define RLO_BF16_LS_MATH 6
 #endif
@@ -297,6 +408,8 @@ cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
   } else if constexpr (NT >= 2 && LOSS && RLO_BF16_LS_U != 0) {  // lockstep on a deferred offset
     return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_LS_MATH | kMathDeferred, RLO_BF16_LS_U, false, true>(a, num_sms, s);
   } else {
+    if constexpr (NT == 1 && LOSS && ENT0 && RLO_BF16_PAIR_U > 0)  // P = 1: two rows per warp
+      return launch_pair<ET, RLO_BF16_PAIR_U, 6>(a, num_sms, s);
     if constexpr (NT == 1 && LOSS && ENT0 && RLO_BF16_MATH_P1 != RLO_BF16_MATH)  // A/B: actor-only loss pass
       return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH_P1, RLO_BF16_U, RLO_BF16_PF>(a, num_sms, s);
     return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, false, RLO_BF16_UN, RLO_BF16_PFN>(

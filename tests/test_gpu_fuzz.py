@@ -187,7 +187,7 @@ def test_random_update_pass_vs_oracle(env, case):
 @pytest.mark.parametrize("case", range(24))
 def test_random_long_rows_loss_pass_vs_oracle(env, case):
     """Long bf16 rows (the lockstep kernels on a deferred offset for P = 2 / 3,
-    the lazy-max kernel for P = 1): random vocabularies >= 64 Ki (odd ones,
+    two rows per warp for P = 1): random vocabularies >= 64 Ki (odd ones,
     padded and unaligned strides), old / ref rows shifted against the actor
     by up to +-90 nats, -inf masked entries, late spikes far above a thread's
     first batch, whole rows shifted by hundreds of nats -- per-token log-probs

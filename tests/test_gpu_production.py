@@ -17,7 +17,8 @@ rlo_objective_step_host_mb):
 * bf16 P = 2: the same lockstep kernel with two tensors; both lockstep
   kernels at V = 32000 too, with old/ref rows far above and far below the
   actor's;
-* bf16 P = 1: the lazy-running-max kernel (mix 7);
+* bf16 P = 1: two rows per warp in lockstep, each on its own deferred offset;
+* bf16 forward_logprobs: the lazy-running-max kernel (mix 7);
 * the fp32 and bf16 forward_logprobs instantiations with and without entropy.
 
 Tolerance (north_star): |gpu - oracle| <= 1e-5 * max(1, |oracle|) for
@@ -394,8 +395,8 @@ def test_bf16_long_lockstep_deferred_offset(env, gap, pad):
 @pytest.mark.parametrize("P", [1, 2])
 def test_bf16_p1_p2_kernels(env, P, V):
     """bf16 loss pass with one or two logits tensors (old / ref log-probs
-    precomputed) against the oracle: P = 1 takes the lazy-running-max kernel
-    (mix 7), P = 2 the lockstep kernel on a deferred offset; at V = 152064 the old rows of the first tokens are
+    precomputed) against the oracle: P = 1 takes the two-rows-per-warp kernel,
+    P = 2 the lockstep kernel, both on deferred offsets; at V = 152064 the old rows of the first tokens are
     the spike rows that defeat a lazy max."""
     torch, rlo, obj = env
     rng = np.random.default_rng(90 + P)
