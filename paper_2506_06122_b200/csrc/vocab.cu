@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(NTH, (LS && sizeof(ET) == 2 ? RLO_BF16_LS_THRE
 // (profiles/r2_vocab_ab.txt calls ax-ay).  A row whose share leaves the safe
 // range (non-finite, or s >= 2^32: the entropy's cancellation) is redone
 // exactly and guarded; a pair with an inactive or misaligned row streams its
-// rows one by one (exact, guarded).
+// rows one by one (the lazy-max stream).
 template <typename ET, int U, int MATH>
 __device__ __forceinline__ void pair_accumulate(const ET* const (&rows)[2], int V, Acc (&acc)[2]) {
   using VT = Vec<ET>;
@@ -284,7 +284,9 @@ __device__ __forceinline__ void pair_accumulate(const ET* const (&rows)[2], int 
     for (int i = nvec * VT::kElems + lane; i < V; i += 32) acc_scalar<ET, true>(rows[k] + i, acc[k]);
 }
 
-template <typename ET, int U, int MATH>
+// MATHS / US / PFS: the single-row stream (lazy max) for a pair with an
+// inactive or misaligned row.
+template <typename ET, int U, int MATH, int MATHS, int US, bool PFS>
 __global__ void __launch_bounds__(32, RLO_BF16_PAIR_THREADS_PER_SM / 32) vocab_pair_kernel(const VocabArgs a) {
   const int lane = threadIdx.x;
   const int64_t nrows = (int64_t)a.B * a.T, npairs = (nrows + 1) / 2;
@@ -316,7 +318,13 @@ __global__ void __launch_bounds__(32, RLO_BF16_PAIR_THREADS_PER_SM / 32) vocab_p
     } else {
 #pragma unroll
       for (int k = 0; k < 2; ++k)
-        if (act[k]) stream_accumulate<32, ET, U, false, true, MATH | kMathGuard>(rp[k], a.V, acc[k]);
+        if (act[k]) {
+          stream_accumulate<32, ET, US, PFS, true, MATHS>(rp[k], a.V, acc[k]);
+          if (!(isfinite(acc[k].s) && isfinite(acc[k].w))) {  // -inf logits: guarded redo
+            acc_init(acc[k]);
+            stream_accumulate<32, ET, US, PFS, true, MATHS | kMathGuard>(rp[k], a.V, acc[k]);
+          }
+        }
     }
 #pragma unroll
     for (int k = 0; k < 2; ++k)
@@ -327,9 +335,9 @@ __global__ void __launch_bounds__(32, RLO_BF16_PAIR_THREADS_PER_SM / 32) vocab_p
   }
 }
 
-template <typename ET, int U, int MATH>
+template <typename ET, int U, int MATH, int MATHS, int US, bool PFS>
 cudaError_t launch_pair(const VocabArgs& a, int num_sms, cudaStream_t s) {
-  auto kern = vocab_pair_kernel<ET, U, MATH>;
+  auto kern = vocab_pair_kernel<ET, U, MATH, MATHS, US, PFS>;
   const int64_t npairs = ((int64_t)a.B * a.T + 1) / 2;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, 0);
@@ -409,7 +417,7 @@ cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
     return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_LS_MATH | kMathDeferred, RLO_BF16_LS_U, false, true>(a, num_sms, s);
   } else {
     if constexpr (NT == 1 && LOSS && ENT0 && RLO_BF16_PAIR_U > 0)  // P = 1: two rows per warp
-      return launch_pair<ET, RLO_BF16_PAIR_U, 6>(a, num_sms, s);
+      return launch_pair<ET, RLO_BF16_PAIR_U, 6, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF>(a, num_sms, s);
     if constexpr (NT == 1 && LOSS && ENT0 && RLO_BF16_MATH_P1 != RLO_BF16_MATH)  // A/B: actor-only loss pass
       return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH_P1, RLO_BF16_U, RLO_BF16_PF>(a, num_sms, s);
     return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, false, RLO_BF16_UN, RLO_BF16_PFN>(
