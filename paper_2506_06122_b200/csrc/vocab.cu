@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(NTH, (LS && sizeof(ET) == 2 ? RLO_BF16_LS_THRE
 // range (non-finite, or s >= 2^32: the entropy's cancellation) is redone
 // exactly and guarded; a pair with an inactive or misaligned row streams its
 // rows one by one (the lazy-max stream).
-template <typename ET, int U, int MATH>
+template <typename ET, int U, int MATH, bool ENT>
 __device__ __forceinline__ void pair_accumulate(const ET* const (&rows)[2], int V, Acc (&acc)[2]) {
   using VT = Vec<ET>;
   using VV = typename VT::V;
@@ -255,9 +255,9 @@ __device__ __forceinline__ void pair_accumulate(const ET* const (&rows)[2], int 
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       if (acc[k].mL > kLazyMin)
-        VT::template accumulate<U, true, MATH | kMathNoMax>(v[k], acc[k]);
+        VT::template accumulate<U, ENT, MATH | kMathNoMax>(v[k], acc[k]);
       else
-        VT::template accumulate<U, true, MATH>(v[k], acc[k]);
+        VT::template accumulate<U, ENT, MATH>(v[k], acc[k]);
     }
   };
   for (int base = 0; base < nfull; base += kStep) {
@@ -281,12 +281,15 @@ __device__ __forceinline__ void pair_accumulate(const ET* const (&rows)[2], int 
   }
 #pragma unroll
   for (int k = 0; k < 2; ++k)
-    for (int i = nvec * VT::kElems + lane; i < V; i += 32) acc_scalar<ET, true>(rows[k] + i, acc[k]);
+    for (int i = nvec * VT::kElems + lane; i < V; i += 32) acc_scalar<ET, ENT>(rows[k] + i, acc[k]);
 }
 
 // MATHS / US / PFS: the single-row stream (lazy max) for a pair with an
 // inactive or misaligned row.
-template <typename ET, int U, int MATH, int MATHS, int US, bool PFS>
+// LOSS / ENT0: the loss pass (P = 1) or forward_logprobs, with or without
+// the entropy (a row without entropy takes the polynomial lanes of MATH and
+// is redone when its share leaves [.., 2^100) on its own offset).
+template <typename ET, int U, int MATH, int MATHS, int US, bool PFS, bool LOSS, bool ENT0>
 __global__ void __launch_bounds__(32, RLO_BF16_PAIR_THREADS_PER_SM / 32) vocab_pair_kernel(const VocabArgs a) {
   const int lane = threadIdx.x;
   const int64_t nrows = (int64_t)a.B * a.T, npairs = (nrows + 1) / 2;
@@ -300,29 +303,29 @@ __global__ void __launch_bounds__(32, RLO_BF16_PAIR_THREADS_PER_SM / 32) vocab_p
     Acc acc[2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      act[k] = r[k] < nrows && row_active<true>(a, r[k], lane == 0);
-      if (r[k] < nrows && !act[k] && lane == 0) write_inactive<true>(a, r[k]);
+      act[k] = r[k] < nrows && row_active<LOSS>(a, r[k], lane == 0);
+      if (r[k] < nrows && !act[k] && lane == 0) write_inactive<LOSS>(a, r[k]);
       if (act[k] && lane == 0) gather_token<ET, 1>(a, r[k], tok[k], oov[k], ztok[k]);
       rp[k] = reinterpret_cast<const ET*>(a.logits[0]) + (r[k] < nrows ? logits_off(a, 0, r[k]) : 0);
       acc_init(acc[k]);
     }
     const bool aligned = ((reinterpret_cast<uintptr_t>(rp[0]) | reinterpret_cast<uintptr_t>(rp[1])) & 15u) == 0;
     if (act[0] && act[1] && aligned) {
-      pair_accumulate<ET, U, MATH>(rp, a.V, acc);
+      pair_accumulate<ET, U, MATH, ENT0>(rp, a.V, acc);
 #pragma unroll
       for (int k = 0; k < 2; ++k)
-        if (!(isfinite(acc[k].s) && isfinite(acc[k].w)) || !(acc[k].s < kLazyCap)) {
+        if (ENT0 ? (!(isfinite(acc[k].s) && isfinite(acc[k].w)) || !(acc[k].s < kLazyCap)) : !(acc[k].s < kDeferCap)) {
           acc_init(acc[k]);
-          stream_accumulate<32, ET, U, false, true, MATH | kMathGuard>(rp[k], a.V, acc[k]);
+          stream_accumulate<32, ET, U, false, ENT0, MATH | (ENT0 ? kMathGuard : 0)>(rp[k], a.V, acc[k]);
         }
     } else {
 #pragma unroll
       for (int k = 0; k < 2; ++k)
         if (act[k]) {
-          stream_accumulate<32, ET, US, PFS, true, MATHS>(rp[k], a.V, acc[k]);
-          if (!(isfinite(acc[k].s) && isfinite(acc[k].w))) {  // -inf logits: guarded redo
+          stream_accumulate<32, ET, US, PFS, ENT0, MATHS>(rp[k], a.V, acc[k]);
+          if (ENT0 && !(isfinite(acc[k].s) && isfinite(acc[k].w))) {  // -inf logits: guarded redo
             acc_init(acc[k]);
-            stream_accumulate<32, ET, US, PFS, true, MATHS | kMathGuard>(rp[k], a.V, acc[k]);
+            stream_accumulate<32, ET, US, PFS, ENT0, MATHS | kMathGuard>(rp[k], a.V, acc[k]);
           }
         }
     }
@@ -330,14 +333,14 @@ __global__ void __launch_bounds__(32, RLO_BF16_PAIR_THREADS_PER_SM / 32) vocab_p
     for (int k = 0; k < 2; ++k)
       if (act[k]) {
         Acc c[1] = {acc[k]};
-        row_finish_acc<1, true, true>(a, c, r[k], tok[k], oov[k], ztok[k], lane);
+        row_finish_acc<1, LOSS, ENT0>(a, c, r[k], tok[k], oov[k], ztok[k], lane);
       }
   }
 }
 
-template <typename ET, int U, int MATH, int MATHS, int US, bool PFS>
+template <typename ET, int U, int MATH, int MATHS, int US, bool PFS, bool LOSS, bool ENT0>
 cudaError_t launch_pair(const VocabArgs& a, int num_sms, cudaStream_t s) {
-  auto kern = vocab_pair_kernel<ET, U, MATH, MATHS, US, PFS>;
+  auto kern = vocab_pair_kernel<ET, U, MATH, MATHS, US, PFS, LOSS, ENT0>;
   const int64_t npairs = ((int64_t)a.B * a.T + 1) / 2;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, 0);
@@ -401,6 +404,9 @@ cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
 #ifndef RLO_BF16_LS_U  // lockstep vectors per tensor per batch (0: per-tensor lazy streams, A/B)
 #define RLO_BF16_LS_U 3
 #endif
+#ifndef RLO_BF16_PAIR_FWD  // forward_logprobs through the pair kernel too (A/B)
+#define RLO_BF16_PAIR_FWD 0
+#endif
 #ifndef RLO_BF16_PAIR_U  // 0: the lazy-max stream (A/B)
 #define RLO_BF16_PAIR_U 5
 #endif
@@ -417,7 +423,9 @@ cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
     return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_LS_MATH | kMathDeferred, RLO_BF16_LS_U, false, true>(a, num_sms, s);
   } else {
     if constexpr (NT == 1 && LOSS && ENT0 && RLO_BF16_PAIR_U > 0)  // P = 1: two rows per warp
-      return launch_pair<ET, RLO_BF16_PAIR_U, 6, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF>(a, num_sms, s);
+      return launch_pair<ET, RLO_BF16_PAIR_U, 6, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, true, true>(a, num_sms, s);
+    if constexpr (NT == 1 && !LOSS && RLO_BF16_PAIR_FWD && RLO_BF16_PAIR_U > 0)  // A/B: forward_logprobs in pairs
+      return launch_pair<ET, RLO_BF16_PAIR_U, 6, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, false, ENT0>(a, num_sms, s);
     if constexpr (NT == 1 && LOSS && ENT0 && RLO_BF16_MATH_P1 != RLO_BF16_MATH)  // A/B: actor-only loss pass
       return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH_P1, RLO_BF16_U, RLO_BF16_PF>(a, num_sms, s);
     return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, false, RLO_BF16_UN, RLO_BF16_PFN>(
