@@ -1,4 +1,5 @@
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -rf 2>&1 | tail -2
-timeout 900 python bench.py > gpurun_out/r2k_bench_cfg3.json 2> gpurun_out/r2k_bench_cfg3.err; python3 -c "
-import json; d=json.loads(open('gpurun_out/r2k_bench_cfg3.json').read().strip().splitlines()[0]); r=d['roofline']; p=d['p1']
-print(round(d['value']/1e6,3), round(r['achieved']), round(r['frac'],3), d['clocks']['sm_mhz'], round(p['value']/1e6,2), round(p['achieved_gbs']), r['traffic'])"
+RLO_LIB=$PWD/paper_2506_06122_b200/lib/variants/librlo_pfwd.so timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider -rf 2>&1 | tail -2
+for r in 1 2 3; do for L in cur pfwd; do RLO_LIB=$PWD/paper_2506_06122_b200/lib/variants/librlo_$L.so timeout 300 python tools/bench_fwd.py 2>/dev/null | python3 -c "
+import json,sys
+for l in sys.stdin:
+    d=json.loads(l); print('$L r$r', 'entropy', d['entropy'], round(d['ms'],3), 'ms', round(d['gbs']), 'GB/s')"; done; done | tee gpurun_out/r2az_fwd.txt

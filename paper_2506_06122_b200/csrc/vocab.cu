@@ -235,8 +235,8 @@ __global__ void __launch_bounds__(NTH, (LS && sizeof(ET) == 2 ? RLO_BF16_LS_THRE
   }
 }
 
-// The bf16 1-tensor loss pass (P = 1: old / ref log-probs precomputed): TWO
-// rows per warp in lockstep (consecutive tokens), U = 5 vectors of each per
+// The bf16 1-tensor passes (the P = 1 loss pass: old / ref log-probs
+// precomputed; forward_logprobs, +4%, call az): TWO rows per warp in lockstep (consecutive tokens), U = 5 vectors of each per
 // batch, each row on its own deferred offset (the max of its first batch),
 // 768 resident threads per SM: +2.9% over the lazy-max stream with prefetch
 // (profiles/r2_vocab_ab.txt calls ax-ay).  A row whose share leaves the safe
@@ -377,9 +377,10 @@ cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
 //        pairs, the entropy row all MUFU): +3-4% over per-tensor lazy-max
 //        streams on Qwen rows, +7% over the round-2 short-row lockstep
 //        (shared running max, U = 2) on V = 32000 rows (profiles/r2_vocab_ab.txt);
-//  bf16 P = 1 loss pass: two rows per warp in lockstep (vocab_pair_kernel);
-//  bf16 forward_logprobs: mix 7 = mix 6 + the lazy running max, U = 4 with
-//        the next batch in flight (software prefetch), one warp per row.
+//  bf16 P = 1 loss pass and forward_logprobs: two rows per warp in lockstep
+//        (vocab_pair_kernel); a pair with an inactive or misaligned row
+//        streams them one by one: mix 7 = mix 6 + the lazy running max, U = 4
+//        with the next batch in flight (software prefetch).
 #ifndef RLO_F32_MATH
 #define RLO_F32_MATH 1
 #endif
@@ -404,8 +405,8 @@ cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
 #ifndef RLO_BF16_LS_U  // lockstep vectors per tensor per batch (0: per-tensor lazy streams, A/B)
 #define RLO_BF16_LS_U 3
 #endif
-#ifndef RLO_BF16_PAIR_FWD  // forward_logprobs through the pair kernel too (A/B)
-#define RLO_BF16_PAIR_FWD 0
+#ifndef RLO_BF16_PAIR_FWD  // forward_logprobs through the pair kernel too: +4% (call az)
+#define RLO_BF16_PAIR_FWD 1
 #endif
 #ifndef RLO_BF16_PAIR_U  // 0: the lazy-max stream (A/B)
 #define RLO_BF16_PAIR_U 5
@@ -424,7 +425,7 @@ cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
   } else {
     if constexpr (NT == 1 && LOSS && ENT0 && RLO_BF16_PAIR_U > 0)  // P = 1: two rows per warp
       return launch_pair<ET, RLO_BF16_PAIR_U, 6, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, true, true>(a, num_sms, s);
-    if constexpr (NT == 1 && !LOSS && RLO_BF16_PAIR_FWD && RLO_BF16_PAIR_U > 0)  // A/B: forward_logprobs in pairs
+    if constexpr (NT == 1 && !LOSS && RLO_BF16_PAIR_FWD && RLO_BF16_PAIR_U > 0)  // forward_logprobs in pairs
       return launch_pair<ET, RLO_BF16_PAIR_U, 6, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, false, ENT0>(a, num_sms, s);
     if constexpr (NT == 1 && LOSS && ENT0 && RLO_BF16_MATH_P1 != RLO_BF16_MATH)  // A/B: actor-only loss pass
       return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH_P1, RLO_BF16_U, RLO_BF16_PF>(a, num_sms, s);
