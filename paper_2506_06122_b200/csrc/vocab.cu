@@ -422,11 +422,9 @@ cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
     return launch_ldg<ET, NT, LOSS, ENT0, RLO_F32_MATH, 8, false>(a, num_sms, s);
   } else if constexpr (NT >= 2 && LOSS && RLO_BF16_LS_U != 0) {  // lockstep on a deferred offset
     return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_LS_MATH | kMathDeferred, RLO_BF16_LS_U, false, true>(a, num_sms, s);
+  } else if constexpr (NT == 1 && RLO_BF16_PAIR_U > 0 && (LOSS || RLO_BF16_PAIR_FWD)) {  // two rows per warp
+    return launch_pair<ET, RLO_BF16_PAIR_U, 6, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, LOSS, ENT0>(a, num_sms, s);
   } else {
-    if constexpr (NT == 1 && LOSS && ENT0 && RLO_BF16_PAIR_U > 0)  // P = 1: two rows per warp
-      return launch_pair<ET, RLO_BF16_PAIR_U, 6, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, true, true>(a, num_sms, s);
-    if constexpr (NT == 1 && !LOSS && RLO_BF16_PAIR_FWD && RLO_BF16_PAIR_U > 0)  // forward_logprobs in pairs
-      return launch_pair<ET, RLO_BF16_PAIR_U, 6, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, false, ENT0>(a, num_sms, s);
     if constexpr (NT == 1 && LOSS && ENT0 && RLO_BF16_MATH_P1 != RLO_BF16_MATH)  // A/B: actor-only loss pass
       return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH_P1, RLO_BF16_U, RLO_BF16_PF>(a, num_sms, s);
     return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_MATH, RLO_BF16_U, RLO_BF16_PF, false, RLO_BF16_UN, RLO_BF16_PFN>(

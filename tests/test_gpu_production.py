@@ -17,8 +17,9 @@ rlo_objective_step_host_mb):
 * bf16 P = 2: the same lockstep kernel with two tensors; both lockstep
   kernels at V = 32000 too, with old/ref rows far above and far below the
   actor's;
-* bf16 P = 1: two rows per warp in lockstep, each on its own deferred offset;
-* bf16 forward_logprobs: the lazy-running-max kernel (mix 7);
+* bf16 P = 1 and forward_logprobs: two rows per warp in lockstep, each on its
+  own deferred offset (a pair with an inactive or misaligned row: the
+  lazy-running-max stream, mix 7);
 * the fp32 and bf16 forward_logprobs instantiations with and without entropy.
 
 Tolerance (north_star): |gpu - oracle| <= 1e-5 * max(1, |oracle|) for
