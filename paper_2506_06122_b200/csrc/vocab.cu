@@ -351,143 +351,6 @@ cudaError_t launch_pair(const VocabArgs& a, int num_sms, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// A/B (RLO_BF16_PAIR_LS_U > 0): the P >= 2 lockstep with TWO tokens per warp
-// (2 x NT streams), each token on its own deferred offset.
-template <typename ET, int NT, int U, int MATH>
-__device__ __forceinline__ void pair_ls_accumulate(const ET* const (&rows)[2][NT], int V, Acc (&acc)[2][NT]) {
-  using VT = Vec<ET>;
-  using VV = typename VT::V;
-  constexpr int kStep = 32 * U;
-  const int lane = threadIdx.x & 31;
-  const int nvec = V / VT::kElems;
-  const int nfull = nvec / kStep * kStep;
-  auto step = [&](const VV (&v)[2][NT][U]) {
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      if (!(acc[j][0].mL > kLazyMin)) {  // the token's first batch: exact, sets the shared offset
-        const float newmL = __fmul_rn(VT::template chunk_max<U>(v[j][0]), kL2E);
-        if (newmL > acc[j][0].mL) {
-          const float d = acc[j][0].mL - newmL, sc = ex2(d);
-          acc[j][0].w = (acc[j][0].w + acc[j][0].s * d) * sc;
-#pragma unroll
-          for (int k = 0; k < NT; ++k) {
-            acc[j][k].s *= sc;
-            acc[j][k].mL = newmL;
-          }
-        }
-      }
-      VT::template accumulate<U, true, MATH | kMathNoMax>(v[j][0], acc[j][0]);
-#pragma unroll
-      for (int k = 1; k < NT; ++k) VT::template accumulate<U, false, MATH | kMathNoMax>(v[j][k], acc[j][k]);
-    }
-  };
-  for (int base = 0; base < nfull; base += kStep) {
-    VV v[2][NT][U];
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int k = 0; k < NT; ++k)
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          v[j][k][u] = ld_stream(reinterpret_cast<const VV*>(rows[j][k]) + base + u * 32 + lane);
-    step(v);
-  }
-  if (nfull < nvec) {
-    VV v[2][NT][U];
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int k = 0; k < NT; ++k)
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int idx = nfull + u * 32 + lane;
-          v[j][k][u] = idx < nvec ? ld_stream(reinterpret_cast<const VV*>(rows[j][k]) + idx) : VT::fill();
-        }
-    step(v);
-  }
-#pragma unroll
-  for (int j = 0; j < 2; ++j)
-#pragma unroll
-    for (int k = 0; k < NT; ++k)
-      for (int i = nvec * VT::kElems + lane; i < V; i += 32) {
-        if (k == 0)
-          acc_scalar<ET, true>(rows[j][k] + i, acc[j][k]);
-        else
-          acc_scalar<ET, false>(rows[j][k] + i, acc[j][k]);
-      }
-}
-
-template <typename ET, int NT, int U, int MATH, int LSU>
-__global__ void __launch_bounds__(32, RLO_BF16_LS_THREADS_PER_SM / 32) vocab_pair_ls_kernel(const VocabArgs a) {
-  const int lane = threadIdx.x;
-  const int64_t nrows = (int64_t)a.B * a.T, npairs = (nrows + 1) / 2;
-  for (int64_t pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
-    const int64_t r[2] = {2 * pr, 2 * pr + 1};
-    bool act[2], al[2];
-    int tok[2] = {0, 0};
-    bool oov[2] = {false, false};
-    float ztok[2][NT];
-    const ET* rows[2][NT];
-    Acc acc[2][NT];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      act[j] = r[j] < nrows && row_active<true>(a, r[j], lane == 0);
-      if (r[j] < nrows && !act[j] && lane == 0) write_inactive<true>(a, r[j]);
-      if (act[j] && lane == 0) gather_token<ET, NT>(a, r[j], tok[j], oov[j], ztok[j]);
-      al[j] = true;
-#pragma unroll
-      for (int k = 0; k < NT; ++k) {
-        rows[j][k] = reinterpret_cast<const ET*>(a.logits[k]) + (r[j] < nrows ? logits_off(a, k, r[j]) : 0);
-        al[j] &= (reinterpret_cast<uintptr_t>(rows[j][k]) & 15u) == 0;
-        acc_init(acc[j][k]);
-      }
-    }
-    if (act[0] && act[1] && al[0] && al[1]) {
-      pair_ls_accumulate<ET, NT, U, MATH>(rows, a.V, acc);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        if (!act[j]) continue;
-        if (al[j]) {
-          lockstep_accumulate<32, ET, NT, LSU, MATH, true>(rows[j], a.V, acc[j]);
-        } else {
-          stream_accumulate<32, ET, LSU, false, true, MATH | kMathGuard>(rows[j][0], a.V, acc[j][0]);
-#pragma unroll
-          for (int k = 1; k < NT; ++k) stream_accumulate<32, ET, LSU, false, false, MATH>(rows[j][k], a.V, acc[j][k]);
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      if (!act[j]) continue;
-      if (!(isfinite(acc[j][0].s) && isfinite(acc[j][0].w)) || !(acc[j][0].s < kLazyCap)) {
-        acc_init(acc[j][0]);
-        stream_accumulate<32, ET, LSU, false, true, MATH | kMathGuard>(rows[j][0], a.V, acc[j][0]);
-      }
-#pragma unroll
-      for (int k = 1; k < NT; ++k)
-        if (!(acc[j][k].s >= 0x1p-80f && acc[j][k].s < 0x1p100f)) {
-          acc_init(acc[j][k]);
-          stream_accumulate<32, ET, LSU, false, false, MATH>(rows[j][k], a.V, acc[j][k]);
-        }
-      row_finish_acc<NT, true, true>(a, acc[j], r[j], tok[j], oov[j], ztok[j], lane);
-    }
-  }
-}
-
-template <typename ET, int NT, int U, int MATH, int LSU>
-cudaError_t launch_pair_ls(const VocabArgs& a, int num_sms, cudaStream_t s) {
-  auto kern = vocab_pair_ls_kernel<ET, NT, U, MATH, LSU>;
-  const int64_t npairs = ((int64_t)a.B * a.T + 1) / 2;
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, 0);
-  int64_t grid = (int64_t)num_sms * (per_sm < 1 ? 1 : per_sm);
-  if (grid > npairs) grid = npairs;
-  kern<<<(int)grid, 32, 0, s>>>(a);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
-}
-
 template <typename ET, int NT, bool LOSS, bool ENT0, int MATH, int U, bool PF, bool LS = false, int UN = U,
           bool PFN = PF>
 cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
@@ -548,9 +411,6 @@ cudaError_t launch_ldg(const VocabArgs& a, int num_sms, cudaStream_t s) {
 #ifndef RLO_BF16_PAIR_U  // 0: the lazy-max stream (A/B)
 #define RLO_BF16_PAIR_U 5
 #endif
-#ifndef RLO_BF16_PAIR_LS_U
-#define RLO_BF16_PAIR_LS_U 0
-#endif
 #ifndef RLO_BF16_LS_MATH
 #define RLO_BF16_LS_MATH 6
 #endif
@@ -560,8 +420,6 @@ cudaError_t launch_any(const VocabArgs& a, int num_sms, cudaStream_t s) {
   if ((int64_t)a.B * a.T == 0) return cudaSuccess;
   if constexpr (sizeof(ET) == 4) {
     return launch_ldg<ET, NT, LOSS, ENT0, RLO_F32_MATH, 8, false>(a, num_sms, s);
-  } else if constexpr (NT >= 2 && LOSS && RLO_BF16_LS_U != 0 && RLO_BF16_PAIR_LS_U > 0) {  // A/B: 2 tokens per warp
-    return launch_pair_ls<ET, NT, RLO_BF16_PAIR_LS_U, RLO_BF16_LS_MATH, RLO_BF16_LS_U>(a, num_sms, s);
   } else if constexpr (NT >= 2 && LOSS && RLO_BF16_LS_U != 0) {  // lockstep on a deferred offset
     return launch_ldg<ET, NT, LOSS, ENT0, RLO_BF16_LS_MATH | kMathDeferred, RLO_BF16_LS_U, false, true>(a, num_sms, s);
   } else if constexpr (NT == 1 && RLO_BF16_PAIR_U > 0 && (LOSS || RLO_BF16_PAIR_FWD)) {  // two rows per warp
